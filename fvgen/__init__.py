@@ -1,0 +1,89 @@
+"""Seeded synthetic inputs for GPU-FV tests and benchmarks (SURVEY.md §8(d) recipe).
+
+This module holds NONE of the method's arithmetic (no log-likelihoods, posteriors, statistics or
+normalisation); it only draws GMMs and descriptor sets.  It is the one module both the oracle side
+(tests, bench cpu_baseline) and the CUDA side (tests, bench) use.  Everything is float32, row-major,
+exactly what the C-ABI consumes; the oracle converts the same float32 values to double.
+
+Recipe (post-PCA-like descriptors, P:138 / P:449):
+  per-dimension spread     s_k = 0.5 (k+1)^(-1/2)                      (decaying PCA spectrum)
+  priors                   pi ~ Dirichlet(2 * 1_K)
+  means                    mu_jk = s_k sqrt(f) N(0,1)                  (f = between-cluster fraction)
+  std-devs                 sd_jk = s_k sqrt(1-f) U(0.7, 1.3)           (variances = sd^2 go to the ABI)
+  descriptors              c_i ~ Cat(pi), x_i = mu_{c_i} + sd_{c_i} * N(0, I); the first 5 % are
+                           replaced by background N(0, diag s^2); then the rows are shuffled.
+Acceptance set: f = 0.3.  Stress sets: f = 0.15 ("flat") and "peaked" (sd = s U(0.3, 0.7), mu = s N).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SEED_GMM = 1604
+
+
+def spread(D: int) -> np.ndarray:
+    return 0.5 * (np.arange(D, dtype=np.float64) + 1.0) ** -0.5
+
+
+def make_gmm(K: int, D: int, seed: int = SEED_GMM, f: float = 0.3, kind: str = "acceptance"):
+    """Return (priors[K], means[K,D], variances[K,D]) as float32 (variances = sigma^2, reading A1)."""
+    rng = np.random.default_rng(seed)
+    s = spread(D)
+    pi = rng.dirichlet(2.0 * np.ones(K))
+    if kind == "peaked":
+        mu = s * rng.standard_normal((K, D))
+        sd = s * rng.uniform(0.3, 0.7, (K, D))
+    else:
+        mu = s * np.sqrt(f) * rng.standard_normal((K, D))
+        sd = s * np.sqrt(1.0 - f) * rng.uniform(0.7, 1.3, (K, D))
+    pi = pi.astype(np.float32)
+    # guarantee strictly positive float32 priors (Dirichlet draws can be tiny but never exactly 0)
+    pi = np.maximum(pi, np.float32(1e-30))
+    return pi, mu.astype(np.float32), (sd * sd).astype(np.float32)
+
+
+def make_descriptors(gmm, N: int, seed: int, bg_frac: float = 0.05) -> np.ndarray:
+    """N x D float32 descriptors drawn from the GMM (+ background), shuffled."""
+    pi, mu, var = gmm
+    K, D = mu.shape
+    rng = np.random.default_rng(seed)
+    if N == 0:
+        return np.zeros((0, D), dtype=np.float32)
+    p = pi.astype(np.float64)
+    c = rng.choice(K, size=N, p=p / p.sum())
+    sd = np.sqrt(var.astype(np.float64))
+    x = mu[c].astype(np.float64) + sd[c] * rng.standard_normal((N, D))
+    nb = int(round(bg_frac * N))
+    if nb:
+        x[:nb] = spread(D) * rng.standard_normal((nb, D))
+    rng.shuffle(x, axis=0)
+    return x.astype(np.float32)
+
+
+def voc_counts(B: int, seed: int, mean: int = 20000) -> np.ndarray:
+    """C3: ragged per-image descriptor counts round(mean * U(0.75, 1.25))."""
+    rng = np.random.default_rng(seed)
+    return np.round(mean * rng.uniform(0.75, 1.25, B)).astype(np.int64)
+
+
+def make_batch(gmm, counts, seed_base: int):
+    """Concatenate independently seeded images; returns (X[n_total, D] float32, offsets[B+1] int64)."""
+    counts = np.asarray(counts, dtype=np.int64)
+    D = gmm[1].shape[1]
+    offsets = np.zeros(len(counts) + 1, dtype=np.int64)
+    offsets[1:] = np.cumsum(counts)
+    X = np.empty((int(offsets[-1]), D), dtype=np.float32)
+    for b, n in enumerate(counts):
+        X[offsets[b]:offsets[b + 1]] = make_descriptors(gmm, int(n), seed_base + b)
+    return X, offsets
+
+
+# Named configurations from BASELINE.json "configs".
+CONFIGS = {
+    "C1": dict(K=16, D=64, counts=[1000], seed_gmm=1604, seed_data=1605),
+    "C2": dict(K=256, D=64, counts=[5000], seed_gmm=1604, seed_data=1604 + 1000),
+    "C2_paper_geometry": dict(K=256, D=64, counts=[17714], seed_gmm=1604, seed_data=1604 + 1000),
+    "C3": dict(K=256, D=64, B=256, mean=20000, seed_gmm=1604, seed_data=1604 + 10000),
+    "C4": dict(K=256, D=64, frames=4096, per_frame=5000, seed_gmm=1604, seed_data=1604 + 20000),
+    "C5": dict(K=512, D=128, counts=[10_000_000], seed_gmm=1605, seed_data=1605 + 1),
+}

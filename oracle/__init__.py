@@ -1,0 +1,25 @@
+"""CPU double-precision oracle for GPU-FV Fisher-vector encoding (arXiv 1604.03498).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, ``__graft_entry__.smoke()`` and bench.py's
+``cpu_baseline`` / ``--impl reference`` legs.  The product package (paper_1604_03498_b200) never
+imports it, and it never imports the product package.  See oracle/fv_oracle.c for the arithmetic and
+the PAPER.md passages each function follows.
+
+Parity status: every function here is pinned by tests/test_oracle.py (closed forms, invariants,
+mpmath brute force); none is "parity unpinned".
+"""
+from .oracle import (  # noqa: F401
+    NORM_IMPROVED,
+    NORM_NONE,
+    NORM_POWER_L2,
+    accumulate,
+    build,
+    encode,
+    encode_batched,
+    fv_from_stats,
+    max_threads,
+    normalize,
+    posteriors,
+    stats,
+    stats_batched,
+)

@@ -1,0 +1,186 @@
+"""ctypes wrapper around oracle/fv_oracle.c (TEST INFRASTRUCTURE ONLY — see oracle/__init__.py).
+
+Inputs are converted to float64 exactly (the GPU path receives the same float32 values), outputs are
+float64 numpy arrays.  The library is built with plain ``gcc -O2 -fopenmp`` (no -ffast-math) on first
+use, or by ``__graft_entry__.build()``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+NORM_IMPROVED = 0
+NORM_POWER_L2 = 1
+NORM_NONE = 2
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "fv_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+def build(force: bool = False) -> str:
+    """Compile fv_oracle.c into oracle/liboracle.so (IEEE double, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared",
+             "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build())
+            lib.fvo_posteriors.argtypes = [_dp, ctypes.c_int64, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int, _dp]
+            lib.fvo_posteriors.restype = None
+            lib.fvo_accumulate.argtypes = [_dp, ctypes.c_int64, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int,
+                                           ctypes.c_double, _dp, _dp]
+            lib.fvo_accumulate.restype = None
+            lib.fvo_normalize.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _dp, ctypes.c_int]
+            lib.fvo_normalize.restype = None
+            lib.fvo_encode.argtypes = [_dp, ctypes.c_int64, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int,
+                                       ctypes.c_double, ctypes.c_int, _dp, _dp]
+            lib.fvo_encode.restype = ctypes.c_int
+            lib.fvo_encode_batched.argtypes = [_dp, _i64p, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp,
+                                               ctypes.c_int, ctypes.c_double, ctypes.c_int, _dp, ctypes.c_int]
+            lib.fvo_encode_batched.restype = ctypes.c_int
+            lib.fvo_stats.argtypes = [_dp, ctypes.c_int64, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int,
+                                      ctypes.c_double, _dp]
+            lib.fvo_stats.restype = ctypes.c_int
+            lib.fvo_stats_batched.argtypes = [_dp, _i64p, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp,
+                                              ctypes.c_int, ctypes.c_double, _dp, ctypes.c_int]
+            lib.fvo_stats_batched.restype = ctypes.c_int
+            lib.fvo_max_threads.argtypes = []
+            lib.fvo_max_threads.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _d(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _gmm(priors, means, variances):
+    w, m, v = _d(priors), _d(means), _d(variances)
+    K = w.shape[0]
+    assert m.ndim == 2 and m.shape[0] == K and v.shape == m.shape
+    return w, m, v, K, m.shape[1]
+
+
+def max_threads() -> int:
+    return int(_load().fvo_max_threads())
+
+
+def posteriors(X, priors, means, variances) -> np.ndarray:
+    """Alg.1 lines 2-15: gamma (N x K) in double precision."""
+    w, m, v, K, D = _gmm(priors, means, variances)
+    X = _d(X).reshape(-1, D)
+    g = np.empty((X.shape[0], K), dtype=np.float64)
+    _load().fvo_posteriors(_p(X), X.shape[0], D, _p(w), _p(m), _p(v), K, _p(g))
+    return g
+
+
+def accumulate(X, gamma, means, variances, threshold: float = 0.0):
+    """Alg.1 lines 16-26: raw (U, V), each K x D."""
+    m, v = _d(means), _d(variances)
+    K, D = m.shape
+    X = _d(X).reshape(-1, D)
+    g = _d(gamma).reshape(X.shape[0], K)
+    U = np.zeros((K, D)); V = np.zeros((K, D))
+    _load().fvo_accumulate(_p(X), X.shape[0], D, _p(g), _p(m), _p(v), K, float(threshold), _p(U), _p(V))
+    return U, V
+
+
+def normalize(fv, priors, N: int, mode: int = NORM_IMPROVED) -> np.ndarray:
+    """Reading A9 on fv = [U, V] (length 2KD)."""
+    w = _d(priors)
+    K = w.shape[0]
+    fv = _d(fv).copy().reshape(-1)
+    D = fv.shape[0] // (2 * K)
+    _load().fvo_normalize(_p(fv), K, D, int(N), _p(w), int(mode))
+    return fv
+
+
+def encode(X, priors, means, variances, threshold: float = 0.0, mode: int = NORM_IMPROVED,
+           return_gamma: bool = False):
+    """Full encode of one descriptor set -> FV (2KD,) [and gamma (N x K)]."""
+    w, m, v, K, D = _gmm(priors, means, variances)
+    X = _d(X).reshape(-1, D)
+    fv = np.empty(2 * K * D)
+    g = np.empty((X.shape[0], K)) if return_gamma else None
+    rc = _load().fvo_encode(_p(X), X.shape[0], D, _p(w), _p(m), _p(v), K, float(threshold), int(mode),
+                            _p(fv), _p(g) if g is not None else None)
+    if rc != 0:
+        raise MemoryError("fvo_encode failed")
+    return (fv, g) if return_gamma else fv
+
+
+def encode_batched(X, offsets, priors, means, variances, threshold: float = 0.0,
+                   mode: int = NORM_IMPROVED, nthreads: int = 0) -> np.ndarray:
+    """Independent images (CSR offsets, length batch+1) -> (batch, 2KD).  OpenMP over images."""
+    w, m, v, K, D = _gmm(priors, means, variances)
+    X = _d(X).reshape(-1, D)
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    B = off.shape[0] - 1
+    assert off[0] == 0 and off[-1] == X.shape[0]
+    out = np.empty((B, 2 * K * D))
+    rc = _load().fvo_encode_batched(_p(X), off.ctypes.data_as(_i64p), B, D, _p(w), _p(m), _p(v), K,
+                                    float(threshold), int(mode), _p(out), int(nthreads))
+    if rc != 0:
+        raise MemoryError("fvo_encode_batched failed")
+    return out
+
+
+def stats(X, priors, means, variances, threshold: float = 0.0) -> np.ndarray:
+    """[N, S0 (K), S1 (KxD), S2 (KxD)] about c = sum_j pi_j mu_j / sum_j pi_j (reading A19)."""
+    w, m, v, K, D = _gmm(priors, means, variances)
+    X = _d(X).reshape(-1, D)
+    s = np.empty(1 + K * (2 * D + 1))
+    if _load().fvo_stats(_p(X), X.shape[0], D, _p(w), _p(m), _p(v), K, float(threshold), _p(s)) != 0:
+        raise MemoryError("fvo_stats failed")
+    return s
+
+
+def stats_batched(X, offsets, priors, means, variances, threshold: float = 0.0, nthreads: int = 0):
+    w, m, v, K, D = _gmm(priors, means, variances)
+    X = _d(X).reshape(-1, D)
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    B = off.shape[0] - 1
+    s = np.empty((B, 1 + K * (2 * D + 1)))
+    rc = _load().fvo_stats_batched(_p(X), off.ctypes.data_as(_i64p), B, D, _p(w), _p(m), _p(v), K,
+                                   float(threshold), _p(s), int(nthreads))
+    if rc != 0:
+        raise MemoryError("fvo_stats_batched failed")
+    return s
+
+
+def fv_from_stats(st, priors, means, variances, mode: int = NORM_IMPROVED) -> np.ndarray:
+    """FV from summed statistics (the descriptor-sharded path's finalize, written plainly):
+    U = (S1 - mu' S0)/sd, V = (S2 - 2 mu' S1 + mu'^2 S0)/var - S0, mu' = mu - c, then normalize."""
+    w, m, v, K, D = _gmm(priors, means, variances)
+    st = _d(st)
+    N = int(round(st[0]))
+    S0 = st[1:1 + K]
+    S1 = st[1 + K:1 + K + K * D].reshape(K, D)
+    S2 = st[1 + K + K * D:].reshape(K, D)
+    c = (w[:, None] * m).sum(0) / w.sum()
+    mp = m - c[None, :]
+    U = (S1 - mp * S0[:, None]) / np.sqrt(v)
+    V = (S2 - 2 * mp * S1 + mp * mp * S0[:, None]) / v - S0[:, None]
+    return normalize(np.concatenate([U.ravel(), V.ravel()]), w, N, mode)
