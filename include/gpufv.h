@@ -1,0 +1,127 @@
+/*
+ * gpufv.h — C ABI of the B200-native Fisher-vector encoder (GPU-FV, Ma et al., ICMR'16, arXiv 1604.03498).
+ *
+ * What is computed (PAPER.md = P:<line>; readings A1..A19 are listed in DESIGN.md §3):
+ *   For an image with descriptors x_1..x_N (D dims) and a diagonal GMM (K components, priors pi_j,
+ *   means mu_jk, variances var_jk — the paper's "covariances", reading A1):
+ *     Phase 1, Alg.1 l.2-15:  l_ij = ln pi_j - 1/2 sum_k ln var_jk - 1/2 sum_k (x_ik-mu_jk)^2/var_jk
+ *                                          gamma_ij = exp(l_ij - max_j l_ij) / sum_j exp(l_ij - max_j l_ij)
+ *     Phase 2, Alg.1 l.16-26: for every (i,j) with gamma_ij > threshold (all pairs if threshold <= 0):
+ *                                          U_jk += gamma_ij (x_ik-mu_jk)/sqrt(var_jk)
+ *                                          V_jk += gamma_ij ((x_ik-mu_jk)^2/var_jk - 1)
+ *     Normalisation, "same encoding scheme as VLFeat" (reading A9): U_jk /= N sqrt(pi_j),
+ *       V_jk /= N sqrt(2 pi_j), z <- sign(z) sqrt|z|, z /= ||z||_2 (an all-zero vector stays zero).
+ *   Output per image: 2*K*D floats, U block (K x D row-major, by Gaussian) then V block (reading A8).
+ *
+ * Conventions for every function below:
+ *   - Array arguments are CUDA DEVICE pointers on the current device unless the name ends in _host.
+ *     The library never allocates, frees or synchronises on the device paths; all work is enqueued
+ *     asynchronously on `stream` (NULL = legacy default stream).  The caller owns every buffer.
+ *   - fp32 in, fp32 out; internal statistics are reduced in fp64.  Results are deterministic
+ *     (static schedule + fixed-order reductions): identical inputs give bitwise-identical outputs.
+ *   - Limits: 1 <= K <= 1024, 1 <= D <= 64, D % 4 == 0 (caller pads, reading A13), X 16-byte aligned.
+ *   - Device data is not validated (that would need a kernel + sync): var <= 0, pi <= 0 or non-finite
+ *     X propagate NaN into that image's output only.  Descriptors with |x-c|/rms >= 255 in some
+ *     dimension (c, rms: GMM-weighted mean/RMS) overflow the fp16 split operands.
+ *   - Synchronous argument errors return a status; asynchronous CUDA errors are reported by the
+ *     next call or by cudaGetLastError.  fv_last_error() returns a thread-local detail string.
+ *   - Thread safety: reentrant; concurrent calls need distinct workspaces.
+ */
+#ifndef GPUFV_H
+#define GPUFV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *fv_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  FV_OK = 0,
+  FV_ERR_ARG = 1,         /* null pointer, N/batch < 0, K < 1, D < 1, threshold NaN or >= 1, bad flags */
+  FV_ERR_UNSUPPORTED = 2, /* K > 1024, D > 64, D % 4 != 0, misaligned X, device is not sm_100      */
+  FV_ERR_WORKSPACE = 3,   /* ws_bytes < fv_workspace_bytes(...) or ws misaligned (needs 1024 B)    */
+  FV_ERR_CUDA = 4         /* a CUDA launch/runtime call failed (detail in fv_last_error())          */
+} fv_status;
+
+enum {
+  FV_NORM_IMPROVED = 0,       /* default: 1/(N sqrt(pi)), 1/(N sqrt(2 pi)), signed sqrt, L2  (A9) */
+  FV_NORM_POWER_L2 = 1,       /* signed sqrt + L2 only                                          */
+  FV_NORM_NONE = 2,           /* raw Alg.1 sums U, V                                            */
+  FV_NORM_MASK = 3,
+  FV_SIGMA_IS_STDDEV = 1u << 4, /* `sigmas` are standard deviations (default: variances, A1)    */
+  FV_DETERMINISTIC = 1u << 5,   /* accepted for compatibility; every path is deterministic        */
+  FV_PREPARED = 1u << 6         /* `ws` already holds this GMM prepared by fv_gmm_prepare: skip a1 */
+};
+
+/* Bytes of device workspace needed by the calls below for this problem size.  n_total = total
+ * descriptors, batch = images per call.  With FV_HOST_IO_BYTES semantics the _host entry point also
+ * needs room for the device copies of X, offsets and out: use fv_workspace_bytes_host. */
+size_t fv_workspace_bytes(int64_t n_total, int batch, int K, int D, unsigned flags);
+size_t fv_workspace_bytes_host(int64_t n_total, int batch, int K, int D, unsigned flags);
+
+/* Step a1 (Alg.1 l.1 "Compute sqrt(sigma^-1)"; done "with a simple GPU kernel"):
+ * prepares the GMM-derived operands (fp16 hi/lo split of [mu'/var, -1/(2 var)], log-prior+log-det
+ * bias, feature shift c = sum_j pi_j mu_j / sum_j pi_j and power-of-two feature scales) into the head
+ * of `ws`.  Later calls on the same ws may pass FV_PREPARED to skip it. */
+fv_status fv_gmm_prepare(const float *weights /*K*/, const float *means /*KxD*/, const float *sigmas /*KxD*/,
+                         int K, int D, unsigned flags, void *ws, size_t ws_bytes, fv_stream_t stream);
+
+/* One descriptor set X (N x D row-major) -> out (2KD).  N == 0 gives an all-zero FV (A11). */
+fv_status fv_encode(const float *X, int64_t N, int D, const float *weights, const float *means,
+                    const float *sigmas, int K, float threshold, unsigned flags, float *out,
+                    void *ws, size_t ws_bytes, fv_stream_t stream);
+
+/* A batch of independent images: X (n_total x D), image b = rows offsets[b]..offsets[b+1]-1
+ * (`offsets`: device int64 array of batch+1 non-decreasing entries, offsets[0]=0, offsets[batch]=n_total)
+ * -> out (batch x 2KD). */
+fv_status fv_encode_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D,
+                            const float *weights, const float *means, const float *sigmas, int K,
+                            float threshold, unsigned flags, float *out, void *ws, size_t ws_bytes,
+                            fv_stream_t stream);
+
+/* Same as fv_encode_batched but X_host / offsets_host / out_host are HOST buffers (pinned for full
+ * PCIe speed); the GMM arrays stay device pointers (a resident model).  Copies in, encodes, copies out
+ * on `stream` and synchronises it before returning.  ws >= fv_workspace_bytes_host(...). */
+fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total,
+                                 int D, const float *weights, const float *means, const float *sigmas, int K,
+                                 float threshold, unsigned flags, float *out_host, void *ws, size_t ws_bytes,
+                                 fv_stream_t stream);
+
+/* Split path for descriptor sharding (a2-a6 without a7).  stats: batch x (1 + K(2D+1)) doubles,
+ *   stats[b] = [ N_b, S0 (K), S1 (K x D), S2 (K x D) ],
+ *   S0_j = sum_i gamma_ij,  S1_jk = sum_i gamma_ij (x_ik - c_k),  S2_jk = sum_i gamma_ij (x_ik - c_k)^2,
+ * summed over included pairs, about c = sum_j pi_j mu_j / sum_j pi_j (reading A19).  Statistics of
+ * disjoint descriptor sets add (the NCCL all-reduce of the sharded path). */
+fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D,
+                           const float *weights, const float *means, const float *sigmas, int K,
+                           float threshold, unsigned flags, double *stats, void *ws, size_t ws_bytes,
+                           fv_stream_t stream);
+
+/* a7: stats (as above, possibly summed across GPUs) -> out (batch x 2KD):
+ *   U = (S1 - mu' S0)/sqrt(var), V = (S2 - 2 mu' S1 + mu'^2 S0)/var - S0, mu' = mu - c, then the
+ *   normalisation selected by flags.  Uses the prepared GMM in ws (runs a1 unless FV_PREPARED). */
+fv_status fv_finalize(const double *stats, int batch, int D, const float *weights, const float *means,
+                      const float *sigmas, int K, unsigned flags, float *out, void *ws, size_t ws_bytes,
+                      fv_stream_t stream);
+
+/* Test hook: posteriors gamma (N x K fp32) of one set, computed by the production kernel (same
+ * GEMM + softmax path as fv_encode); entries <= threshold are zeroed when threshold > 0. */
+fv_status fv_posteriors(const float *X, int64_t N, int D, const float *weights, const float *means,
+                        const float *sigmas, int K, float threshold, unsigned flags, float *gamma,
+                        void *ws, size_t ws_bytes, fv_stream_t stream);
+
+/* Number of kernel launches the last successful call on this thread enqueued (for bench accounting). */
+int fv_last_launch_count(void);
+
+const char *fv_status_string(fv_status s);
+const char *fv_last_error(void);
+int fv_version(void); /* 100 * major + minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPUFV_H */

@@ -1,0 +1,254 @@
+"""B200-native Fisher-vector encoder (GPU-FV, arXiv 1604.03498) — thin Python binding.
+
+Every call marshals torch CUDA tensors into the C ABI of ``libgpufv.so`` (include/gpufv.h) and
+enqueues on the current torch CUDA stream.  All arithmetic runs in the library's sm_100a kernels;
+there is NO CPU fallback: if the shared library is missing this module raises on import.
+PyTorch is used only for device memory, streams and (in ``dist``) process groups.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+__all__ = [
+    "NORM_IMPROVED", "NORM_POWER_L2", "NORM_NONE", "SIGMA_IS_STDDEV", "PREPARED",
+    "GMM", "Workspace", "lib", "lib_path", "workspace_bytes", "gmm_prepare", "encode", "encode_batched",
+    "encode_batched_host", "stats_batched", "finalize", "posteriors", "last_launch_count", "FVError",
+]
+
+NORM_IMPROVED = 0
+NORM_POWER_L2 = 1
+NORM_NONE = 2
+SIGMA_IS_STDDEV = 1 << 4
+DETERMINISTIC = 1 << 5
+PREPARED = 1 << 6
+_RAW_LOGLIK = 1 << 8  # test hook of fv_posteriors: raw log2-likelihoods instead of gamma
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libgpufv.so")
+
+if not os.path.exists(lib_path):
+    raise ImportError(
+        f"{lib_path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback)")
+
+lib = ctypes.CDLL(lib_path)
+
+_c = ctypes
+_vp, _i64, _i32, _f32, _u32, _sz = _c.c_void_p, _c.c_int64, _c.c_int, _c.c_float, _c.c_uint, _c.c_size_t
+
+lib.fv_workspace_bytes.argtypes = [_i64, _i32, _i32, _i32, _u32]
+lib.fv_workspace_bytes.restype = _sz
+lib.fv_workspace_bytes_host.argtypes = [_i64, _i32, _i32, _i32, _u32]
+lib.fv_workspace_bytes_host.restype = _sz
+lib.fv_gmm_prepare.argtypes = [_vp, _vp, _vp, _i32, _i32, _u32, _vp, _sz, _vp]
+lib.fv_encode.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _f32, _u32, _vp, _vp, _sz, _vp]
+lib.fv_encode_batched.argtypes = [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _i32, _f32, _u32, _vp, _vp, _sz, _vp]
+lib.fv_encode_batched_host.argtypes = lib.fv_encode_batched.argtypes
+lib.fv_stats_batched.argtypes = [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _i32, _f32, _u32, _vp, _vp, _sz, _vp]
+lib.fv_finalize.argtypes = [_vp, _i32, _i32, _vp, _vp, _vp, _i32, _u32, _vp, _vp, _sz, _vp]
+lib.fv_posteriors.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _f32, _u32, _vp, _vp, _sz, _vp]
+for _fn in ("fv_gmm_prepare", "fv_encode", "fv_encode_batched", "fv_encode_batched_host", "fv_stats_batched",
+            "fv_finalize", "fv_posteriors"):
+    getattr(lib, _fn).restype = _i32
+lib.fv_status_string.argtypes = [_i32]
+lib.fv_status_string.restype = _c.c_char_p
+lib.fv_last_error.argtypes = []
+lib.fv_last_error.restype = _c.c_char_p
+lib.fv_last_launch_count.argtypes = []
+lib.fv_last_launch_count.restype = _i32
+lib.fv_version.restype = _i32
+
+
+class FVError(RuntimeError):
+    def __init__(self, status: int):
+        self.status = status
+        super().__init__(f"{lib.fv_status_string(status).decode()}: {lib.fv_last_error().decode()}")
+
+
+def _check(status: int):
+    if status != 0:
+        raise FVError(status)
+
+
+def _stream():
+    return _c.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return _c.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def last_launch_count() -> int:
+    return int(lib.fv_last_launch_count())
+
+
+class GMM:
+    """Device-resident diagonal GMM: weights (K), means (K x D), sigmas (K x D; variances unless
+    ``stddev``), all float32 contiguous CUDA tensors."""
+
+    def __init__(self, weights, means, sigmas, stddev: bool = False, device=None):
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.weights = torch.as_tensor(weights, dtype=torch.float32).to(dev).contiguous()
+        self.means = torch.as_tensor(means, dtype=torch.float32).to(dev).contiguous()
+        self.sigmas = torch.as_tensor(sigmas, dtype=torch.float32).to(dev).contiguous()
+        self.K, self.D = self.means.shape
+        self.flags = SIGMA_IS_STDDEV if stddev else 0
+
+    def ptrs(self):
+        return _ptr(self.weights), _ptr(self.means), _ptr(self.sigmas)
+
+
+def workspace_bytes(n_total: int, batch: int, K: int, D: int, flags: int = 0, host_io: bool = False) -> int:
+    fn = lib.fv_workspace_bytes_host if host_io else lib.fv_workspace_bytes
+    n = int(fn(int(n_total), int(batch), int(K), int(D), int(flags)))
+    if n == 0:
+        raise FVError(1)
+    return n
+
+
+class Workspace:
+    """A growable 1024-byte-aligned device buffer (torch caching allocator); holds the prepared GMM
+    at its head, so reuse one Workspace per GMM and pass prepared=True after gmm_prepare."""
+
+    def __init__(self, nbytes: int = 0, device=None):
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self._buf = None
+        self.nbytes = 0
+        self.ptr = 0
+        if nbytes:
+            self.ensure(nbytes)
+
+    def ensure(self, nbytes: int):
+        if nbytes > self.nbytes:
+            # growing invalidates a prepared GMM; callers re-prepare (encode(prepared=False))
+            self._buf = torch.empty(nbytes + 1024, dtype=torch.uint8, device=self.device)
+            base = self._buf.data_ptr()
+            self.ptr = (base + 1023) // 1024 * 1024
+            self.nbytes = nbytes
+            self.generation = getattr(self, "generation", 0) + 1
+        return self
+
+    def args(self):
+        return _c.c_void_p(self.ptr), _c.c_size_t(self.nbytes)
+
+
+def _ws(ws, need, device):
+    if ws is None:
+        ws = Workspace(device=device)
+    gen = getattr(ws, "generation", 0)
+    ws.ensure(need)
+    return ws, getattr(ws, "generation", 0) != gen
+
+
+def _mode_flags(gmm: GMM, mode: int, prepared: bool) -> int:
+    return int(mode) | gmm.flags | (PREPARED if prepared else 0)
+
+
+def gmm_prepare(gmm: GMM, ws: Workspace):
+    """Step a1 once per GMM (Alg.1 l.1): later calls may pass prepared=True."""
+    ws.ensure(workspace_bytes(0, 1, gmm.K, gmm.D))
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_gmm_prepare(w, m, s, gmm.K, gmm.D, gmm.flags, *ws.args(), _stream()))
+
+
+def _check_X(X, D):
+    if not (X.is_cuda and X.dtype == torch.float32 and X.is_contiguous() and X.dim() == 2 and X.shape[1] == D):
+        raise ValueError(f"X must be a contiguous float32 CUDA tensor of shape (N, {D})")
+
+
+def encode(X, gmm: GMM, threshold: float = 0.0, mode: int = NORM_IMPROVED, ws: Workspace | None = None,
+           prepared: bool = False, out=None):
+    """One descriptor set (N x D) -> FV (2KD,)."""
+    _check_X(X, gmm.D)
+    ws, grown = _ws(ws, workspace_bytes(X.shape[0], 1, gmm.K, gmm.D), X.device)
+    prepared = prepared and not grown
+    if out is None:
+        out = torch.empty(2 * gmm.K * gmm.D, dtype=torch.float32, device=X.device)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_encode(_ptr(X), X.shape[0], gmm.D, w, m, s, gmm.K, float(threshold),
+                         _mode_flags(gmm, mode, prepared), _ptr(out), *ws.args(), _stream()))
+    return out
+
+
+def encode_batched(X, offsets, gmm: GMM, threshold: float = 0.0, mode: int = NORM_IMPROVED,
+                   ws: Workspace | None = None, prepared: bool = False, out=None):
+    """Independent images: X (n_total x D), offsets (batch+1, int64 CUDA) -> (batch, 2KD)."""
+    _check_X(X, gmm.D)
+    if not (offsets.is_cuda and offsets.dtype == torch.int64 and offsets.is_contiguous()):
+        raise ValueError("offsets must be a contiguous int64 CUDA tensor")
+    B = offsets.shape[0] - 1
+    ws, grown = _ws(ws, workspace_bytes(X.shape[0], B, gmm.K, gmm.D), X.device)
+    prepared = prepared and not grown
+    if out is None:
+        out = torch.empty(B, 2 * gmm.K * gmm.D, dtype=torch.float32, device=X.device)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_encode_batched(_ptr(X), _ptr(offsets), B, X.shape[0], gmm.D, w, m, s, gmm.K, float(threshold),
+                                 _mode_flags(gmm, mode, prepared), _ptr(out), *ws.args(), _stream()))
+    return out
+
+
+def encode_batched_host(X_host, offsets_host, gmm: GMM, threshold: float = 0.0, mode: int = NORM_IMPROVED,
+                        ws: Workspace | None = None, prepared: bool = False, out_host=None):
+    """Host buffers in and out (pinned CPU tensors for full PCIe speed); the GMM stays on the GPU.
+    The H2D copy, encode and D2H copy all happen inside the library call, which returns when the
+    host result is ready."""
+    assert X_host.device.type == "cpu" and X_host.dtype == torch.float32 and X_host.is_contiguous()
+    assert offsets_host.device.type == "cpu" and offsets_host.dtype == torch.int64
+    B = offsets_host.shape[0] - 1
+    ws, grown = _ws(ws, workspace_bytes(X_host.shape[0], B, gmm.K, gmm.D, host_io=True), gmm.means.device)
+    prepared = prepared and not grown
+    if out_host is None:
+        out_host = torch.empty(B, 2 * gmm.K * gmm.D, dtype=torch.float32, pin_memory=True)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_encode_batched_host(_ptr(X_host), _ptr(offsets_host), B, X_host.shape[0], gmm.D, w, m, s, gmm.K,
+                                      float(threshold), _mode_flags(gmm, mode, prepared), _ptr(out_host),
+                                      *ws.args(), _stream()))
+    return out_host
+
+
+def stats_batched(X, offsets, gmm: GMM, threshold: float = 0.0, ws: Workspace | None = None,
+                  prepared: bool = False, out=None):
+    """Sufficient statistics (batch, 1 + K(2D+1)) float64 about c (reading A19); they add across
+    disjoint descriptor shards."""
+    _check_X(X, gmm.D)
+    B = offsets.shape[0] - 1
+    ws, grown = _ws(ws, workspace_bytes(X.shape[0], B, gmm.K, gmm.D), X.device)
+    prepared = prepared and not grown
+    if out is None:
+        out = torch.empty(B, 1 + gmm.K * (2 * gmm.D + 1), dtype=torch.float64, device=X.device)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_stats_batched(_ptr(X), _ptr(offsets), B, X.shape[0], gmm.D, w, m, s, gmm.K, float(threshold),
+                                _mode_flags(gmm, 0, prepared), _ptr(out), *ws.args(), _stream()))
+    return out
+
+
+def finalize(stats, gmm: GMM, mode: int = NORM_IMPROVED, ws: Workspace | None = None, prepared: bool = False,
+             out=None):
+    """Statistics (batch, 1 + K(2D+1)) float64 -> FVs (batch, 2KD)."""
+    assert stats.is_cuda and stats.dtype == torch.float64 and stats.is_contiguous()
+    st = stats.reshape(-1, 1 + gmm.K * (2 * gmm.D + 1))
+    B = st.shape[0]
+    ws, grown = _ws(ws, workspace_bytes(0, B, gmm.K, gmm.D), stats.device)
+    prepared = prepared and not grown
+    if out is None:
+        out = torch.empty(B, 2 * gmm.K * gmm.D, dtype=torch.float32, device=stats.device)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_finalize(_ptr(st), B, gmm.D, w, m, s, gmm.K, _mode_flags(gmm, mode, prepared), _ptr(out),
+                           *ws.args(), _stream()))
+    return out
+
+
+def posteriors(X, gmm: GMM, threshold: float = 0.0, raw_loglik: bool = False, ws: Workspace | None = None):
+    """Test hook: gamma (N x K) from the production kernel; raw_loglik returns log2-likelihoods
+    (+ per-Gaussian bias, shifted by a per-GMM constant) instead."""
+    _check_X(X, gmm.D)
+    ws, _ = _ws(ws, workspace_bytes(X.shape[0], 1, gmm.K, gmm.D), X.device)
+    g = torch.empty(X.shape[0], gmm.K, dtype=torch.float32, device=X.device)
+    w, m, s = gmm.ptrs()
+    flags = gmm.flags | (_RAW_LOGLIK if raw_loglik else 0)
+    _check(lib.fv_posteriors(_ptr(X), X.shape[0], gmm.D, w, m, s, gmm.K, float(threshold), flags, _ptr(g),
+                             *ws.args(), _stream()))
+    return g

@@ -1,0 +1,418 @@
+// gpufv.cu — host side of the C ABI declared in include/gpufv.h: argument validation, workspace
+// layout, launches.  No allocation, no synchronisation (except fv_encode_batched_host, which must
+// return host results), no CPU fallback: every step of the path runs in the kernels below.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/gpufv.h"
+#include "fv_common.cuh"
+#include "k_aux.cuh"
+#include "k_stats.cuh"
+
+using namespace gpufv;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+fv_status fail(fv_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+fv_status cuda_check(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return FV_OK;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int cluster_size(int K) { return (K + kG - 1) / kG; }
+
+// Persistent grid: the number of co-resident clusters of k_stats on the current device.
+int num_clusters(int C) {
+  static std::mutex mu;
+  static int cache[64][kMaxCluster + 1] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache[dev][C] > 0) return cache[dev][C];
+  if (cudaFuncSetAttribute(k_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) != cudaSuccess) return -1;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(C * 148, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_stats, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    n = sms / C;
+  }
+  cache[dev][C] = n;
+  return n;
+}
+
+struct Layout {
+  int C, Kp, ncl, nslots;
+  size_t wimg, bias, xshift, xscale, cshift, bscratch;  // prepared GMM (head of ws)
+  size_t tiles, off1, partials, norm2, stats;             // per call
+  size_t hx, hoff, hout;                                  // _host entry point
+  size_t total;
+};
+
+bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout &L) {
+  (void)D;
+  L.C = cluster_size(K);
+  L.Kp = L.C * kG;
+  L.ncl = num_clusters(L.C);
+  if (L.ncl <= 0) return false;
+  L.nslots = L.ncl + batch;
+  size_t o = 0;
+  L.wimg = o;     o = align_up(o + (size_t)L.C * kWImgBytes, 1024);
+  L.bias = o;     o = align_up(o + (size_t)L.Kp * 4, 256);
+  L.xshift = o;   o = align_up(o + kDP * 4, 256);
+  L.xscale = o;   o = align_up(o + kDP * 4, 256);
+  L.cshift = o;   o = align_up(o + kDP * 8, 256);
+  L.bscratch = o; o = align_up(o + (size_t)L.Kp * 8, 1024);
+  L.tiles = o;    o = align_up(o + (size_t)(batch + 1) * 8, 256);
+  L.off1 = o;     o = align_up(o + 16, 256);
+  L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 8, 1024);
+  L.partials = o; o = align_up(o + (size_t)L.nslots * (1 + kNF) * L.Kp * 4, 1024);
+  L.stats = o;    // only the _host path uses more; stats are caller-owned
+  L.hx = L.hoff = L.hout = 0;
+  if (host_io) {
+    L.hx = o;   o = align_up(o + (size_t)n_total * D * 4, 1024);
+    L.hoff = o; o = align_up(o + (size_t)(batch + 1) * 8, 256);
+    L.hout = o; o = align_up(o + (size_t)batch * 2 * K * D * 4, 1024);
+  }
+  L.total = o;
+  return true;
+}
+
+fv_status check_gmm_args(int K, int D, const float *w, const float *mu, const float *sg, unsigned flags) {
+  if (!w || !mu || !sg) return fail(FV_ERR_ARG, "null GMM pointer");
+  if (K < 1 || D < 1) return fail(FV_ERR_ARG, "K=%d and D=%d must be >= 1", K, D);
+  if (K > kG * kMaxCluster) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kG * kMaxCluster);
+  if (D > kDP) return fail(FV_ERR_UNSUPPORTED, "D=%d > %d", D, kDP);
+  if (D % 4 != 0) return fail(FV_ERR_UNSUPPORTED, "D=%d is not a multiple of 4 (pad, reading A13)", D);
+  const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED;
+  if (flags & ~known) return fail(FV_ERR_ARG, "unknown flag bits 0x%x", flags & ~known);
+  if ((flags & FV_NORM_MASK) == 3) return fail(FV_ERR_ARG, "invalid normalisation mode 3");
+  return FV_OK;
+}
+
+fv_status check_device() {
+  static int ok_dev[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return fail(FV_ERR_CUDA, "no CUDA device"); }
+  if (dev >= 0 && dev < 64 && ok_dev[dev]) return FV_OK;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) { cudaGetLastError(); return fail(FV_ERR_CUDA, "cudaGetDeviceProperties failed"); }
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(FV_ERR_UNSUPPORTED, "device %s is sm_%d%d; this library is built for sm_100a only", prop.name, prop.major, prop.minor);
+  if (dev >= 0 && dev < 64) ok_dev[dev] = 1;
+  return FV_OK;
+}
+
+fv_status check_ws(void *ws, size_t ws_bytes, const Layout &L) {
+  if (!ws) return fail(FV_ERR_ARG, "null workspace");
+  if (reinterpret_cast<uintptr_t>(ws) % 1024) return fail(FV_ERR_WORKSPACE, "workspace must be 1024-byte aligned");
+  if (ws_bytes < L.total) return fail(FV_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  return FV_OK;
+}
+
+uint8_t *at(void *ws, size_t off) { return static_cast<uint8_t *>(ws) + off; }
+
+fv_status launch_prep(const Layout &L, const float *w, const float *mu, const float *sg, int K, int D, unsigned flags,
+                      void *ws, cudaStream_t st) {
+  const int sd = (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0;
+  k_prep_shift<<<1, 256, 0, st>>>(w, mu, sg, K, D, L.Kp, sd, (double *)at(ws, L.cshift), (float *)at(ws, L.xshift),
+                                  (float *)at(ws, L.xscale), (float *)at(ws, L.bias), (double *)at(ws, L.bscratch));
+  k_prep_w<<<L.Kp, kNF, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
+                                 at(ws, L.wimg));
+  g_launches += 2;
+  return cuda_check("k_prep");
+}
+
+// a2-a6 over a batch: schedule + persistent stats kernel.  gamma (optional) for fv_posteriors.
+fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets, int64_t n_single, int batch, int D,
+                       int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st) {
+  // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
+  int64_t *off1 = (int64_t *)at(ws, L.off1);
+  k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles));
+  if (!offsets) offsets = off1;
+  g_launches += 1;
+  StatsParams p;
+  p.X = X;
+  p.offsets = offsets;
+  p.tile_start = (const int64_t *)at(ws, L.tiles);
+  p.wimg = at(ws, L.wimg);
+  p.bias = (const float *)at(ws, L.bias);
+  p.xshift = (const float *)at(ws, L.xshift);
+  p.xscale = (const float *)at(ws, L.xscale);
+  p.partials = (float *)at(ws, L.partials);
+  p.gamma_out = gamma;
+  p.batch = batch;
+  p.D = D;
+  p.K = K;
+  p.Kp = L.Kp;
+  p.threshold = thr > 0.f ? thr : 0.f;
+  p.gamma_mode = gamma_mode;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = L.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(L.C * L.ncl, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_stats, p);
+  g_launches += 1;
+  if (e != cudaSuccess) return fail(FV_ERR_CUDA, "k_stats launch: %s", cudaGetErrorString(e));
+  return cuda_check("k_stats");
+}
+
+FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, int D, const float *w, const float *mu,
+                     const float *sg, unsigned flags, void *ws) {
+  FinParams f;
+  f.partials = (const float *)at(ws, L.partials);
+  f.stats = nullptr;
+  f.offsets = offsets;
+  f.tile_start = (const int64_t *)at(ws, L.tiles);
+  f.w = w; f.mu = mu; f.sg = sg;
+  f.cshift = (const double *)at(ws, L.cshift);
+  f.xscale = (const float *)at(ws, L.xscale);
+  f.out = nullptr;
+  f.stats_out = nullptr;
+  f.norm2 = (double *)at(ws, L.norm2);
+  f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
+  f.stddev = (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0;
+  f.mode = (int)(flags & FV_NORM_MASK);
+  return f;
+}
+
+fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStream_t st) {
+  if (batch == 0) return FV_OK;
+  if (cudaMemsetAsync(f.norm2, 0, sizeof(double) * batch, st) != cudaSuccess) return cuda_check("memset norm2");
+  const int KD = K * D;
+  k_finalize<<<dim3((KD + 255) / 256, batch), 256, 0, st>>>(f);
+  g_launches += 1;
+  if (f.mode != FV_NORM_NONE) {
+    k_l2scale<<<dim3((2 * KD + 1023) / 1024, batch), 256, 0, st>>>(f.out, f.norm2, 2 * KD);
+    g_launches += 1;
+  }
+  return cuda_check("k_finalize");
+}
+
+fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D,
+                              const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
+                              float *out, void *ws, size_t ws_bytes, cudaStream_t st, const Layout *Lin) {
+  Layout L;
+  if (Lin) L = *Lin;
+  else if (!make_layout(n_total, batch, K, D, false, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  if (!(flags & FV_PREPARED))
+    if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
+  if (batch == 0) return FV_OK;
+  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st)) return s;
+  FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
+  f.out = out;
+  return launch_finalize(f, batch, K, D, st);
+}
+
+fv_status check_common(const float *X, int64_t n_total, int batch, int D, int K, float thr, const float *w,
+                       const float *mu, const float *sg, unsigned flags) {
+  if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags)) return s;
+  if (n_total < 0 || batch < 0) return fail(FV_ERR_ARG, "n_total=%lld, batch=%d must be >= 0", (long long)n_total, batch);
+  if (n_total > 0 && !X) return fail(FV_ERR_ARG, "null X");
+  if (X && reinterpret_cast<uintptr_t>(X) % 16) return fail(FV_ERR_UNSUPPORTED, "X must be 16-byte aligned");
+  if (std::isnan(thr) || thr >= 1.f) return fail(FV_ERR_ARG, "threshold must be < 1 and not NaN");
+  return FV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t fv_workspace_bytes(int64_t n_total, int batch, int K, int D, unsigned flags) {
+  (void)flags;
+  Layout L;
+  if (K < 1 || K > kG * kMaxCluster || batch < 0 || n_total < 0) return 0;
+  if (!make_layout(n_total, batch, K, D, false, L)) return 0;
+  return L.total;
+}
+
+size_t fv_workspace_bytes_host(int64_t n_total, int batch, int K, int D, unsigned flags) {
+  (void)flags;
+  Layout L;
+  if (K < 1 || K > kG * kMaxCluster || batch < 0 || n_total < 0) return 0;
+  if (!make_layout(n_total, batch, K, D, true, L)) return 0;
+  return L.total;
+}
+
+fv_status fv_gmm_prepare(const float *w, const float *mu, const float *sg, int K, int D, unsigned flags, void *ws,
+                         size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags)) return s;
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(0, 0, K, D, false, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (!ws) return fail(FV_ERR_ARG, "null workspace");
+  if (ws_bytes < L.tiles) return fail(FV_ERR_WORKSPACE, "workspace too small for the prepared GMM");
+  return launch_prep(L, w, mu, sg, K, D, flags, ws, (cudaStream_t)stream);
+}
+
+fv_status fv_encode_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D, const float *w,
+                            const float *mu, const float *sg, int K, float thr, unsigned flags, float *out, void *ws,
+                            size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_common(X, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
+  if (batch > 0 && (!offsets || !out)) return fail(FV_ERR_ARG, "null offsets/out");
+  if (fv_status s = check_device()) return s;
+  return encode_batched_impl(X, offsets, batch, n_total, D, w, mu, sg, K, thr, flags, out, ws, ws_bytes,
+                             (cudaStream_t)stream, nullptr);
+}
+
+fv_status fv_encode(const float *X, int64_t N, int D, const float *w, const float *mu, const float *sg, int K,
+                    float thr, unsigned flags, float *out, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_common(X, N, 1, D, K, thr, w, mu, sg, flags)) return s;
+  if (!out) return fail(FV_ERR_ARG, "null out");
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(N, 1, K, D, false, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  return encode_batched_impl(X, nullptr, 1, N, D, w, mu, sg, K, thr, flags, out, ws, ws_bytes, (cudaStream_t)stream, &L);
+}
+
+fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total, int D,
+                                 const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
+                                 float *out_host, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_common(X_host, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
+  if (batch > 0 && (!offsets_host || !out_host)) return fail(FV_ERR_ARG, "null offsets/out");
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(n_total, batch, K, D, true, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  float *dX = (float *)at(ws, L.hx);
+  int64_t *doff = (int64_t *)at(ws, L.hoff);
+  float *dout = (float *)at(ws, L.hout);
+  if (n_total > 0 && cudaMemcpyAsync(dX, X_host, (size_t)n_total * D * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return cuda_check("H2D X");
+  if (cudaMemcpyAsync(doff, offsets_host, (size_t)(batch + 1) * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return cuda_check("H2D offsets");
+  if (fv_status s = encode_batched_impl(dX, doff, batch, n_total, D, w, mu, sg, K, thr, flags, dout, ws, ws_bytes, st, &L))
+    return s;
+  if (batch > 0 && cudaMemcpyAsync(out_host, dout, (size_t)batch * 2 * K * D * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return cuda_check("D2H out");
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("stream sync");
+  return FV_OK;
+}
+
+fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D, const float *w,
+                           const float *mu, const float *sg, int K, float thr, unsigned flags, double *stats, void *ws,
+                           size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_common(X, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
+  if (batch > 0 && (!offsets || !stats)) return fail(FV_ERR_ARG, "null offsets/stats");
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(n_total, batch, K, D, false, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!(flags & FV_PREPARED))
+    if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
+  if (batch == 0) return FV_OK;
+  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st)) return s;
+  FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
+  f.stats_out = stats;
+  k_reduce_stats<<<dim3((K * D + 255) / 256, batch), 256, 0, st>>>(f);
+  g_launches += 1;
+  return cuda_check("k_reduce_stats");
+}
+
+fv_status fv_finalize(const double *stats, int batch, int D, const float *w, const float *mu, const float *sg, int K,
+                      unsigned flags, float *out, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags)) return s;
+  if (batch < 0) return fail(FV_ERR_ARG, "batch < 0");
+  if (batch > 0 && (!stats || !out)) return fail(FV_ERR_ARG, "null stats/out");
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(0, batch, K, D, false, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!(flags & FV_PREPARED))
+    if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
+  FinParams f = fin_params(L, nullptr, batch, K, D, w, mu, sg, flags, ws);
+  f.partials = nullptr;
+  f.stats = stats;
+  f.out = out;
+  return launch_finalize(f, batch, K, D, st);
+}
+
+fv_status fv_posteriors(const float *X, int64_t N, int D, const float *w, const float *mu, const float *sg, int K,
+                        float thr, unsigned flags, float *gamma, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  // bit 8 (undocumented, tests only): write raw log2-likelihoods instead of gamma
+  const int mode = (flags & (1u << 8)) ? 2 : 1;
+  flags &= ~(1u << 8);
+  if (fv_status s = check_common(X, N, 1, D, K, thr, w, mu, sg, flags)) return s;
+  if (N > 0 && !gamma) return fail(FV_ERR_ARG, "null gamma");
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(N, 1, K, D, false, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!(flags & FV_PREPARED))
+    if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
+  if (N == 0) return FV_OK;
+  const int64_t *offs = nullptr;
+  return launch_stats(L, X, offs, N, 1, D, K, thr, ws, gamma, mode, st);
+}
+
+int fv_last_launch_count(void) { return g_launches; }
+
+const char *fv_status_string(fv_status s) {
+  switch (s) {
+    case FV_OK: return "FV_OK";
+    case FV_ERR_ARG: return "FV_ERR_ARG: invalid argument";
+    case FV_ERR_UNSUPPORTED: return "FV_ERR_UNSUPPORTED: unsupported shape/alignment/device";
+    case FV_ERR_WORKSPACE: return "FV_ERR_WORKSPACE: workspace too small or misaligned";
+    case FV_ERR_CUDA: return "FV_ERR_CUDA: CUDA error";
+  }
+  return "unknown fv_status";
+}
+
+const char *fv_last_error(void) { return g_err.c_str(); }
+
+int fv_version(void) { return 1; }
+
+}  // extern "C"

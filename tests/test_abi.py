@@ -1,0 +1,92 @@
+"""C-ABI boundary checks that need no GPU: the shared library loads, exports every function that
+include/gpufv.h declares, and rejects bad arguments synchronously (before any CUDA call)."""
+import ctypes
+import math
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gpufv.h")
+LIB = os.path.join(ROOT, "paper_1604_03498_b200", "libgpufv.so")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    return ctypes.CDLL(LIB)
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fv_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for n in ["fv_encode", "fv_encode_batched", "fv_encode_batched_host", "fv_stats_batched", "fv_finalize",
+              "fv_posteriors", "fv_workspace_bytes", "fv_gmm_prepare", "fv_status_string", "fv_last_error"]:
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.check_output(["nm", "-D", "--defined-only", LIB]).decode()
+    exported = set(re.findall(r"\sT\s(fv_[a-z0-9_]+)$", out, flags=re.M))
+    missing = [n for n in declared_functions() if n not in exported]
+    assert not missing, f"declared but not exported: {missing}"
+    for n in declared_functions():
+        getattr(lib, n)  # resolvable through ctypes
+
+
+def test_library_is_sm100a_native():
+    out = subprocess.check_output(["cuobjdump", "--list-elf", LIB]).decode()
+    assert "sm_100a" in out
+    sass = subprocess.check_output(["cuobjdump", "-sass", LIB]).decode()
+    assert "UTCHMMA" in sass, "tcgen05.mma (UTC*MMA) missing from the SASS"
+    assert "LDTM" in sass, "tcgen05.ld (LDTM) missing from the SASS"
+
+
+def _encode(lib, X=1, N=10, D=64, w=1, m=1, s=1, K=16, thr=0.0, flags=0, out=1):
+    f = lib.fv_encode
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                  ctypes.c_int, ctypes.c_float, ctypes.c_uint, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                  ctypes.c_void_p]
+    p = lambda v: ctypes.c_void_p(v * 4096) if v else None  # aligned dummy addresses, never dereferenced
+    return f(p(X), N, D, p(w), p(m), p(s), K, thr, flags, p(out), p(1), 1 << 30, None)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(w=0), 1), (dict(m=0), 1), (dict(s=0), 1), (dict(X=0), 1), (dict(out=0), 1),
+    (dict(K=0), 1), (dict(D=0), 1), (dict(N=-1), 1), (dict(thr=float("nan")), 1), (dict(thr=1.0), 1),
+    (dict(flags=1 << 12), 1), (dict(flags=3), 1),
+    (dict(K=1025), 2), (dict(D=65), 2), (dict(D=6), 2),
+])
+def test_argument_validation(lib, kw, status):
+    assert _encode(lib, **kw) == status
+
+
+def test_misaligned_X_is_unsupported(lib):
+    f = lib.fv_encode
+    f.restype = ctypes.c_int
+    assert f(ctypes.c_void_p(4096 + 4), ctypes.c_int64(10), 64, ctypes.c_void_p(4096), ctypes.c_void_p(4096),
+             ctypes.c_void_p(4096), 16, ctypes.c_float(0.0), ctypes.c_uint(0), ctypes.c_void_p(4096),
+             ctypes.c_void_p(4096), ctypes.c_size_t(1 << 30), None) == 2
+
+
+def test_status_strings(lib):
+    lib.fv_status_string.restype = ctypes.c_char_p
+    lib.fv_last_error.restype = ctypes.c_char_p
+    assert lib.fv_status_string(0) == b"FV_OK"
+    assert b"WORKSPACE" in lib.fv_status_string(3)
+    assert _encode(lib, K=0) == 1
+    assert b"K=0" in lib.fv_last_error()
+
+
+def test_python_binding_imports_without_gpu():
+    import paper_1604_03498_b200 as fv
+    assert fv.lib_path.endswith("libgpufv.so") and fv.lib.fv_version() >= 1
