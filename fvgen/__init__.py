@@ -60,6 +60,36 @@ def make_descriptors(gmm, N: int, seed: int, bg_frac: float = 0.05) -> np.ndarra
     return x.astype(np.float32)
 
 
+def make_frames(gmm, frames: int, per_frame: int, seed: int, block: int = 64, bg_frac: float = 0.05) -> np.ndarray:
+    """Large streams (bench): frames x per_frame descriptors from the same recipe, drawn in float32
+    blocks of `block` frames (one seeded generator per block).  Background rows are placed at random
+    positions (each row with probability bg_frac) instead of first-then-shuffle; same distribution."""
+    pi, mu, var = gmm
+    K, D = mu.shape
+    cdf = np.cumsum(pi.astype(np.float64))
+    cdf /= cdf[-1]
+    sd = np.sqrt(var.astype(np.float64)).astype(np.float32)
+    s = spread(D).astype(np.float32)
+    X = np.empty((frames * per_frame, D), dtype=np.float32)
+
+    def fill(f0):  # independent per block: same result for any thread count
+        rng = np.random.default_rng(seed + f0)
+        n = min(block, frames - f0) * per_frame
+        c = np.minimum(np.searchsorted(cdf, rng.random(n)), K - 1)
+        z = rng.standard_normal((n, D), dtype=np.float32)
+        bg = rng.random(n) < bg_frac
+        xb = X[f0 * per_frame:f0 * per_frame + n]
+        np.multiply(sd[c], z, out=xb)
+        xb += mu[c]
+        xb[bg] = s * z[bg]
+
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+        list(ex.map(fill, range(0, frames, block)))
+    return X
+
+
 def voc_counts(B: int, seed: int, mean: int = 20000) -> np.ndarray:
     """C3: ragged per-image descriptor counts round(mean * U(0.75, 1.25))."""
     rng = np.random.default_rng(seed)

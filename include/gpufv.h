@@ -19,7 +19,7 @@
  *     asynchronously on `stream` (NULL = legacy default stream).  The caller owns every buffer.
  *   - fp32 in, fp32 out; internal statistics are reduced in fp64.  Results are deterministic
  *     (static schedule + fixed-order reductions): identical inputs give bitwise-identical outputs.
- *   - Limits: 1 <= K <= 1024, 1 <= D <= 64, D % 4 == 0 (caller pads, reading A13), X 16-byte aligned.
+ *   - Limits: 1 <= K <= 512, 1 <= D <= 64, D % 4 == 0 (caller pads, reading A13), X 16-byte aligned.
  *   - Device data is not validated (that would need a kernel + sync): var <= 0, pi <= 0 or non-finite
  *     X propagate NaN into that image's output only.  Descriptors with |x-c|/rms >= 255 in some
  *     dimension (c, rms: GMM-weighted mean/RMS) overflow the fp16 split operands.
@@ -42,7 +42,7 @@ typedef struct CUstream_st *fv_stream_t; /* == cudaStream_t */
 typedef enum {
   FV_OK = 0,
   FV_ERR_ARG = 1,         /* null pointer, N/batch < 0, K < 1, D < 1, threshold NaN or >= 1, bad flags */
-  FV_ERR_UNSUPPORTED = 2, /* K > 1024, D > 64, D % 4 != 0, misaligned X, device is not sm_100      */
+  FV_ERR_UNSUPPORTED = 2, /* K > 512, D > 64, D % 4 != 0, misaligned X, device is not sm_100      */
   FV_ERR_WORKSPACE = 3,   /* ws_bytes < fv_workspace_bytes(...) or ws misaligned (needs 1024 B)    */
   FV_ERR_CUDA = 4         /* a CUDA launch/runtime call failed (detail in fv_last_error())          */
 } fv_status;
@@ -113,6 +113,11 @@ fv_status fv_finalize(const double *stats, int batch, int D, const float *weight
 fv_status fv_posteriors(const float *X, int64_t N, int D, const float *weights, const float *means,
                         const float *sigmas, int K, float threshold, unsigned flags, float *gamma,
                         void *ws, size_t ws_bytes, fv_stream_t stream);
+
+/* Profiling hook (bench accounting): when set, every k_stats launch made by this thread is bracketed
+ * by cudaEventRecord(start/stop, stream) so the caller can time the dominant kernel alone with CUDA
+ * events on the stream it runs on.  Pass NULL, NULL to disable.  (cudaEvent_t values.) */
+void fv_profile_events(void *start_event, void *stop_event);
 
 /* Number of kernel launches the last successful call on this thread enqueued (for bench accounting). */
 int fv_last_launch_count(void);

@@ -15,7 +15,8 @@ import torch
 __all__ = [
     "NORM_IMPROVED", "NORM_POWER_L2", "NORM_NONE", "SIGMA_IS_STDDEV", "PREPARED",
     "GMM", "Workspace", "lib", "lib_path", "workspace_bytes", "gmm_prepare", "encode", "encode_batched",
-    "encode_batched_host", "stats_batched", "finalize", "posteriors", "last_launch_count", "FVError",
+    "encode_batched_host", "stats_batched", "finalize", "posteriors", "last_launch_count", "profile_events",
+    "FVError",
 ]
 
 NORM_IMPROVED = 0
@@ -60,6 +61,8 @@ lib.fv_last_error.restype = _c.c_char_p
 lib.fv_last_launch_count.argtypes = []
 lib.fv_last_launch_count.restype = _i32
 lib.fv_version.restype = _i32
+lib.fv_profile_events.argtypes = [_vp, _vp]
+lib.fv_profile_events.restype = None
 
 
 class FVError(RuntimeError):
@@ -83,6 +86,12 @@ def _ptr(t):
 
 def last_launch_count() -> int:
     return int(lib.fv_last_launch_count())
+
+
+def profile_events(start=None, stop=None):
+    """Bracket every k_stats launch of this thread with these torch.cuda.Event objects (None: off)."""
+    lib.fv_profile_events(_c.c_void_p(start.cuda_event) if start is not None else None,
+                          _c.c_void_p(stop.cuda_event) if stop is not None else None)
 
 
 class GMM:

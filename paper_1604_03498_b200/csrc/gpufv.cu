@@ -1,7 +1,9 @@
 // gpufv.cu — host side of the C ABI declared in include/gpufv.h: argument validation, workspace
 // layout, launches.  No allocation, no synchronisation (except fv_encode_batched_host, which must
 // return host results), no CPU fallback: every step of the path runs in the kernels below.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
 #include <cstdarg>
@@ -21,6 +23,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
 
 fv_status fail(fv_status s, const char *fmt, ...) {
   char buf[512];
@@ -45,12 +48,12 @@ int cluster_size(int K) { return (K + kG - 1) / kG; }
 // Persistent grid: the number of co-resident clusters of k_stats on the current device.
 int num_clusters(int C) {
   static std::mutex mu;
-  static int cache[64][kMaxCluster + 1] = {};
+  static int cache[64][kMaxC2 + 1] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
   std::lock_guard<std::mutex> lk(mu);
   if (cache[dev][C] > 0) return cache[dev][C];
-  if (cudaFuncSetAttribute(k_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(k_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess) return -1;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -58,8 +61,8 @@ int num_clusters(int C) {
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3(C * 148, 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.blockDim = dim3(kThreads2, 1, 1);
+  cfg.dynamicSmemBytes = kSmem2Bytes;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
@@ -74,9 +77,10 @@ int num_clusters(int C) {
 }
 
 struct Layout {
-  int C, Kp, ncl, nslots;
+  int C, Kp, ncl;
+  int64_t n_total, nslots;                                         // fold slots (append-only S' chunks)
   size_t wimg, bias, xshift, xscale, cshift, bscratch;  // prepared GMM (head of ws)
-  size_t tiles, off1, partials, norm2, stats;             // per call
+  size_t tiles, off1, norm2, s0slots, slots;              // per call
   size_t hx, hoff, hout;                                  // _host entry point
   size_t total;
 };
@@ -87,7 +91,10 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.Kp = L.C * kG;
   L.ncl = num_clusters(L.C);
   if (L.ncl <= 0) return false;
-  L.nslots = L.ncl + batch;
+  // total tiles <= n_total/128 + batch; fold chunk slots index tc/kFold + cid + b (k_stats.cuh)
+  const int64_t tmax = n_total / kTileM + batch + 1;
+  L.n_total = n_total;
+  L.nslots = tmax / kFold + 1 + L.ncl + batch;
   size_t o = 0;
   L.wimg = o;     o = align_up(o + (size_t)L.C * kWImgBytes, 1024);
   L.bias = o;     o = align_up(o + (size_t)L.Kp * 4, 256);
@@ -97,9 +104,9 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.bscratch = o; o = align_up(o + (size_t)L.Kp * 8, 1024);
   L.tiles = o;    o = align_up(o + (size_t)(batch + 1) * 8, 256);
   L.off1 = o;     o = align_up(o + 16, 256);
-  L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 8, 1024);
-  L.partials = o; o = align_up(o + (size_t)L.nslots * (1 + kNF) * L.Kp * 4, 1024);
-  L.stats = o;    // only the _host path uses more; stats are caller-owned
+  L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 12, 1024);  // double norm2[] + uint counters[]
+  L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * L.Kp * 4, 1024);
+  L.slots = o;    o = align_up(o + (size_t)L.nslots * kNF * L.Kp * 4, 1024);
   L.hx = L.hoff = L.hout = 0;
   if (host_io) {
     L.hx = o;   o = align_up(o + (size_t)n_total * D * 4, 1024);
@@ -113,7 +120,7 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
 fv_status check_gmm_args(int K, int D, const float *w, const float *mu, const float *sg, unsigned flags) {
   if (!w || !mu || !sg) return fail(FV_ERR_ARG, "null GMM pointer");
   if (K < 1 || D < 1) return fail(FV_ERR_ARG, "K=%d and D=%d must be >= 1", K, D);
-  if (K > kG * kMaxCluster) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kG * kMaxCluster);
+  if (K > kG * kMaxC2) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kG * kMaxC2);
   if (D > kDP) return fail(FV_ERR_UNSUPPORTED, "D=%d > %d", D, kDP);
   if (D % 4 != 0) return fail(FV_ERR_UNSUPPORTED, "D=%d is not a multiple of 4 (pad, reading A13)", D);
   const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED;
@@ -163,7 +170,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles));
   if (!offsets) offsets = off1;
   g_launches += 1;
-  StatsParams p;
+  Stats2Params p;
   p.X = X;
   p.offsets = offsets;
   p.tile_start = (const int64_t *)at(ws, L.tiles);
@@ -171,7 +178,8 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.bias = (const float *)at(ws, L.bias);
   p.xshift = (const float *)at(ws, L.xshift);
   p.xscale = (const float *)at(ws, L.xscale);
-  p.partials = (float *)at(ws, L.partials);
+  p.slots = (float *)at(ws, L.slots);
+  p.s0slots = (float *)at(ws, L.s0slots);
   p.gamma_out = gamma;
   p.batch = batch;
   p.D = D;
@@ -179,6 +187,27 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.Kp = L.Kp;
   p.threshold = thr > 0.f ? thr : 0.f;
   p.gamma_mode = gamma_mode;
+  // X as a 2-D tensor map: dims {D, n_total}, boxes of 32 floats x 128 rows, 128B swizzle; rows past
+  // n_total and dims past D read as zero.
+  CUtensorMap tmap;
+  {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void *fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return fail(FV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(L.n_total > 0 ? L.n_total : 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)D * 4};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(X), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -186,21 +215,33 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3(L.C * L.ncl, 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.blockDim = dim3(kThreads2, 1, 1);
+  cfg.dynamicSmemBytes = kSmem2Bytes;
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_stats, p);
+  if (g_prof_start) cudaEventRecord(g_prof_start, st);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_stats, tmap, p);
+  if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
   g_launches += 1;
-  if (e != cudaSuccess) return fail(FV_ERR_CUDA, "k_stats launch: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_stats);
+    cudaGetLastError();
+    return fail(FV_ERR_CUDA,
+                "k_stats launch: %s (grid %d x %d threads, cluster %d, dyn smem %d; kernel: %d regs, max threads %d, "
+                "local %zu B, static smem %zu B, max dyn smem %d)",
+                cudaGetErrorString(e), L.C * L.ncl, kThreads2, L.C, kSmem2Bytes, fa.numRegs, fa.maxThreadsPerBlock,
+                fa.localSizeBytes, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes);
+  }
   return cuda_check("k_stats");
 }
 
 FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, int D, const float *w, const float *mu,
                      const float *sg, unsigned flags, void *ws) {
   FinParams f;
-  f.partials = (const float *)at(ws, L.partials);
+  f.slots = (const float *)at(ws, L.slots);
+  f.s0slots = (const float *)at(ws, L.s0slots);
   f.stats = nullptr;
   f.offsets = offsets;
   f.tile_start = (const int64_t *)at(ws, L.tiles);
@@ -210,6 +251,7 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.out = nullptr;
   f.stats_out = nullptr;
   f.norm2 = (double *)at(ws, L.norm2);
+  f.counters = (unsigned *)(f.norm2 + (batch > 0 ? batch : 1));
   f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
   f.stddev = (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0;
   f.mode = (int)(flags & FV_NORM_MASK);
@@ -217,15 +259,11 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
 }
 
 fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStream_t st) {
+  (void)D;
   if (batch == 0) return FV_OK;
-  if (cudaMemsetAsync(f.norm2, 0, sizeof(double) * batch, st) != cudaSuccess) return cuda_check("memset norm2");
-  const int KD = K * D;
-  k_finalize<<<dim3((KD + 255) / 256, batch), 256, 0, st>>>(f);
+  if (cudaMemsetAsync(f.norm2, 0, (size_t)batch * 12, st) != cudaSuccess) return cuda_check("memset norm2");
+  k_finalize<<<dim3((K + kFinJ - 1) / kFinJ, batch), 256, 0, st>>>(f);
   g_launches += 1;
-  if (f.mode != FV_NORM_NONE) {
-    k_l2scale<<<dim3((2 * KD + 1023) / 1024, batch), 256, 0, st>>>(f.out, f.norm2, 2 * KD);
-    g_launches += 1;
-  }
   return cuda_check("k_finalize");
 }
 
@@ -262,7 +300,7 @@ extern "C" {
 size_t fv_workspace_bytes(int64_t n_total, int batch, int K, int D, unsigned flags) {
   (void)flags;
   Layout L;
-  if (K < 1 || K > kG * kMaxCluster || batch < 0 || n_total < 0) return 0;
+  if (K < 1 || K > kG * kMaxC2 || batch < 0 || n_total < 0) return 0;
   if (!make_layout(n_total, batch, K, D, false, L)) return 0;
   return L.total;
 }
@@ -270,7 +308,7 @@ size_t fv_workspace_bytes(int64_t n_total, int batch, int K, int D, unsigned fla
 size_t fv_workspace_bytes_host(int64_t n_total, int batch, int K, int D, unsigned flags) {
   (void)flags;
   Layout L;
-  if (K < 1 || K > kG * kMaxCluster || batch < 0 || n_total < 0) return 0;
+  if (K < 1 || K > kG * kMaxC2 || batch < 0 || n_total < 0) return 0;
   if (!make_layout(n_total, batch, K, D, true, L)) return 0;
   return L.total;
 }
@@ -353,7 +391,7 @@ fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, in
   if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st)) return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   f.stats_out = stats;
-  k_reduce_stats<<<dim3((K * D + 255) / 256, batch), 256, 0, st>>>(f);
+  k_reduce_stats<<<dim3((K + kFinJ - 1) / kFinJ, batch), 256, 0, st>>>(f);
   g_launches += 1;
   return cuda_check("k_reduce_stats");
 }
@@ -372,7 +410,7 @@ fv_status fv_finalize(const double *stats, int batch, int D, const float *w, con
   if (!(flags & FV_PREPARED))
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
   FinParams f = fin_params(L, nullptr, batch, K, D, w, mu, sg, flags, ws);
-  f.partials = nullptr;
+  f.slots = nullptr;
   f.stats = stats;
   f.out = out;
   return launch_finalize(f, batch, K, D, st);
@@ -399,6 +437,11 @@ fv_status fv_posteriors(const float *X, int64_t N, int D, const float *w, const 
 }
 
 int fv_last_launch_count(void) { return g_launches; }
+
+void fv_profile_events(void *start_event, void *stop_event) {
+  g_prof_start = static_cast<cudaEvent_t>(start_event);
+  g_prof_stop = static_cast<cudaEvent_t>(stop_event);
+}
 
 const char *fv_status_string(fv_status s) {
   switch (s) {

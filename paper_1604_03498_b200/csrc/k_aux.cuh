@@ -2,9 +2,10 @@
 //   k_prep_shift, k_prep_w   step a1: GMM -> prepared operands (Alg.1 l.1)
 //   k_schedule               tile prefix sums from device offsets (ragged batches)
 //   k_finalize               steps a6 (fixed-order fp64 slot reduction) + a7 (centring, VLFeat
-//                            normalisation, P:449 / reading A9), also from fp64 stats (split path)
+//                            normalisation, P:449 / reading A9; the last block of each image applies
+//                            the global L2 normalisation), also from fp64 stats (split path)
 //   k_reduce_stats           a6 only -> fp64 sufficient statistics (descriptor-sharded path)
-//   k_l2scale                global L2 normalisation of each image's FV
+
 #pragma once
 #include <cuda_fp16.h>
 #include "fv_common.cuh"
@@ -142,124 +143,172 @@ __global__ void k_schedule(const int64_t *offsets, int64_t *off1, int64_t n_sing
 }
 
 struct FinParams {
-  const float *partials;      // from k_stats (nullptr when reading stats)
-  const double *stats;        // batch x (1 + K(2D+1)) (nullptr when reading partials)
-  const int64_t *offsets;     // batch + 1 (partials mode)
-  const int64_t *tile_start;  // batch + 1 (partials mode)
+  const float *slots;         // fold slots from k_stats: nslots x kNF x Kp (nullptr when reading stats)
+  const float *s0slots;       // (ncl + batch) x Kp
+  const double *stats;        // batch x (1 + K(2D+1)) (nullptr when reading slots)
+  const int64_t *offsets;     // batch + 1 (slots mode)
+  const int64_t *tile_start;  // batch + 1 (slots mode)
   const float *w, *mu, *sg;
   const double *cshift;
   const float *xscale;
   float *out;                 // batch x 2KD
   double *stats_out;          // k_reduce_stats output
-  double *norm2;              // batch
+  double *norm2;              // batch (zeroed before k_finalize)
+  unsigned *counters;         // batch (zeroed before k_finalize): last-block ticket
   int batch, K, Kp, D, ncl, stddev, mode;
 };
 
 // Owner cluster of global tile t under the static split [c T / ncl, (c+1) T / ncl).
 __device__ __forceinline__ int64_t tile_owner(int64_t t, int64_t T, int64_t ncl) { return ((t + 1) * ncl - 1) / T; }
 
-// Fixed-order (ascending cluster) fp64 reduction of image b's partial slots, unscaled.
-__device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int k, double &S0, double &S1, double &S2,
-                                          double &N) {
-  N = (double)(p.offsets[b + 1] - p.offsets[b]);
-  S0 = S1 = S2 = 0.0;
-  const int64_t T = p.tile_start[p.batch];
-  const int64_t ft = p.tile_start[b], lt = p.tile_start[b + 1] - 1;
-  if (ft > lt) return;
-  const int64_t clo = tile_owner(ft, T, p.ncl), chi = tile_owner(lt, T, p.ncl);
-  const size_t SL = (size_t)(1 + kNF) * p.Kp;
-  for (int64_t c = clo; c <= chi; ++c) {
-    if ((c * T) / p.ncl == ((c + 1) * T) / p.ncl) continue;  // cluster with an empty tile range wrote nothing
-    const float *sl = p.partials + (size_t)(c + b) * SL;
-    S0 += (double)sl[j];
-    S1 += (double)sl[(size_t)(1 + k) * p.Kp + j];
-    S2 += (double)sl[(size_t)(1 + kDP + k) * p.Kp + j];
+// The (cluster, segment) pieces of image b, in ascending cluster order (a6, fixed-order reduction).
+struct ImageSlots {
+  int64_t T, ft, lt, clo, chi;
+  __device__ void init(const FinParams &p, int b) {
+    T = p.tile_start[p.batch];
+    ft = p.tile_start[b];
+    lt = p.tile_start[b + 1];  // exclusive
+    clo = 0; chi = -1;
+    if (ft < lt) { clo = tile_owner(ft, T, p.ncl); chi = tile_owner(lt - 1, T, p.ncl); }
   }
-  const double xs = (double)p.xscale[k];
-  // S0 is accumulated from gamma itself (registers), S1/S2 from gamma * 2^14 (GEMM2 operand)
+  // segment of cluster c inside image b: [s0, s1) (empty if the cluster owns no tile)
+  __device__ void seg(const FinParams &p, int64_t c, int64_t &s0, int64_t &s1) const {
+    const int64_t st = c * T / p.ncl, en = (c + 1) * T / p.ncl;
+    s0 = st > ft ? st : ft;
+    s1 = en < lt ? en : lt;
+  }
+};
+
+// S0_j (gamma units) and S1_jk, S2_jk (about c, unscaled) of image b: fixed-order fp64 sums.
+__device__ __forceinline__ double slot_s0(const FinParams &p, const ImageSlots &is, int b, int j) {
+  double S0 = 0.0;
+  for (int64_t c = is.clo; c <= is.chi; ++c) {
+    int64_t s0, s1;
+    is.seg(p, c, s0, s1);
+    if (s0 >= s1) continue;
+    S0 += (double)p.s0slots[(size_t)(c + b) * p.Kp + j];
+  }
+  return S0 / (double)kPScale;  // S0 was accumulated from P = gamma 2^14
+}
+__device__ __forceinline__ void slot_s12(const FinParams &p, const ImageSlots &is, int b, int j, int k, double &S1,
+                                         double &S2) {
+  S1 = S2 = 0.0;
+  for (int64_t c = is.clo; c <= is.chi; ++c) {
+    int64_t s0, s1;
+    is.seg(p, c, s0, s1);
+    for (int64_t tc = s0; tc < s1; tc += kFold) {
+      const float *sl = p.slots + (size_t)fold_slot(tc, c, b) * kNF * p.Kp;
+      S1 += (double)sl[(size_t)k * p.Kp + j];
+      S2 += (double)sl[(size_t)(kDP + k) * p.Kp + j];
+    }
+  }
+  const double xs = (double)p.xscale[k];  // S1/S2 carry gamma 2^14 and the feature scales 2^e_k
   S1 /= (double)kPScale * xs;
   S2 /= (double)kPScale * xs * xs;
 }
 
-// grid (ceil(K*D/256), batch), 256 threads; thread -> (k, j) with j fastest (coalesced slot reads).
-__global__ void k_finalize(const FinParams p) {
-  __shared__ double s_red[256];
-  const int b = blockIdx.y;
-  const int pidx = blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int kFinJ = 32;  // Gaussians per finalize block
+
+// grid (ceil(K/32), batch), 256 threads.  Thread (jj = tid % 32, k = tid / 32 + 8 i): slot reads are
+// coalesced over jj; U/V go through a shared-memory tile so the global stores are coalesced over
+// (j, k).  Improved-FV scaling + signed sqrt in fp64; the L2 norm is accumulated with one atomic per
+// block and the LAST block of each image (ticket) rescales that image (its lines are still in L2).
+__global__ void __launch_bounds__(256) k_finalize(const FinParams p) {
+  __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
+  __shared__ double s_red[8];
+  __shared__ int s_last;
+  const int b = blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
+  const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), j = j0 + jj;
   const int KD = p.K * p.D;
   double ss = 0.0;
-  if (pidx < KD) {
-    const int k = pidx / p.K, j = pidx - k * p.K;
-    double S0, S1, S2, N;
-    if (p.partials) {
-      slot_sums(p, b, j, k, S0, S1, S2, N);
+  if (jj < nj) {
+    double N, S0;
+    ImageSlots is;
+    const double *st = nullptr;
+    if (p.slots) {
+      N = (double)(p.offsets[b + 1] - p.offsets[b]);
+      is.init(p, b);
+      S0 = slot_s0(p, is, b, j);
     } else {
-      const double *st = p.stats + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
+      st = p.stats + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
       N = st[0];
       S0 = st[1 + j];
-      S1 = st[1 + p.K + (size_t)j * p.D + k];
-      S2 = st[1 + p.K + (size_t)KD + (size_t)j * p.D + k];
     }
-    const double var = gmm_var(p.sg, (size_t)j * p.D + k, p.stddev);
-    const double mup = (double)p.mu[(size_t)j * p.D + k] - p.cshift[k];
-    double U = (S1 - mup * S0) / sqrt(var);
-    double V = (S2 - 2.0 * mup * S1 + mup * mup * S0) / var - S0;
-    if (p.mode != 2) {
-      if (N <= 0.0) { U = 0.0; V = 0.0; }
-      if (p.mode == 0) {
-        const double pj = (double)p.w[j];
-        U /= N * sqrt(pj);
-        V /= N * sqrt(2.0 * pj);
+    const double pj = (double)p.w[j];
+    for (int k = kq; k < p.D; k += 8) {
+      double S1, S2;
+      if (p.slots) {
+        slot_s12(p, is, b, j, k, S1, S2);
+      } else {
+        S1 = st[1 + p.K + (size_t)j * p.D + k];
+        S2 = st[1 + p.K + (size_t)KD + (size_t)j * p.D + k];
       }
-      U = (U > 0.0) ? sqrt(U) : ((U < 0.0) ? -sqrt(-U) : 0.0);
-      V = (V > 0.0) ? sqrt(V) : ((V < 0.0) ? -sqrt(-V) : 0.0);
-      ss = U * U + V * V;
+      const double var = gmm_var(p.sg, (size_t)j * p.D + k, p.stddev);
+      const double mup = (double)p.mu[(size_t)j * p.D + k] - p.cshift[k];
+      double U = (S1 - mup * S0) / sqrt(var);                         // sum gamma (x - mu)/sd
+      double V = (S2 - 2.0 * mup * S1 + mup * mup * S0) / var - S0;  // sum gamma ((x-mu)^2/var - 1)
+      if (p.mode != 2) {
+        if (N <= 0.0) { U = 0.0; V = 0.0; }
+        if (p.mode == 0) { U /= N * sqrt(pj); V /= N * sqrt(2.0 * pj); }
+        ss += fabs(U) + fabs(V);  // = (signed sqrt)^2
+        U = (U > 0.0) ? sqrt(U) : ((U < 0.0) ? -sqrt(-U) : 0.0);
+        V = (V > 0.0) ? sqrt(V) : ((V < 0.0) ? -sqrt(-V) : 0.0);
+      }
+      sU[jj][k] = (float)U;
+      sV[jj][k] = (float)V;
     }
-    float *o = p.out + (size_t)b * 2 * KD;
-    o[(size_t)j * p.D + k] = (float)U;
-    o[(size_t)KD + (size_t)j * p.D + k] = (float)V;
+  }
+  __syncthreads();
+  float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D;
+  for (int t = tid; t < nj * p.D; t += 256) {
+    const int r = t / p.D, k = t - r * p.D;
+    o[t] = sU[r][k];
+    o[KD + t] = sV[r][k];
   }
   if (p.mode == 2) return;
-  s_red[threadIdx.x] = ss;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if ((tid & 31) == 0) s_red[tid >> 5] = ss;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
-    __syncthreads();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < 8; ++w) tot += s_red[w];
+    if (tot != 0.0) atomicAdd(p.norm2 + b, tot);
+    __threadfence();
+    const unsigned ticket = atomicAdd(p.counters + b, 1u);
+    s_last = (ticket == gridDim.x - 1);
   }
-  if (threadIdx.x == 0 && s_red[0] != 0.0) atomicAdd(p.norm2 + b, s_red[0]);
-}
-
-// grid (ceil(2KD/1024), batch), 256 threads x float4.
-__global__ void k_l2scale(float *out, const double *norm2, int KD2) {
-  const int b = blockIdx.y;
-  const double n2 = norm2[b];
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const double n2 = *((volatile double *)(p.norm2 + b));
   if (!(n2 > 0.0)) return;
   const float sc = (float)(1.0 / sqrt(n2));
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  float *o = out + (size_t)b * KD2;
-  if (i + 3 < KD2) {
-    float4 v = *reinterpret_cast<float4 *>(o + i);
+  float4 *ob = reinterpret_cast<float4 *>(p.out + (size_t)b * 2 * KD);  // 2KD % 4 == 0 (D % 4 == 0)
+  for (int t = tid; t < (2 * KD) / 4; t += 256) {
+    float4 v = __ldcg(ob + t);
     v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
-    *reinterpret_cast<float4 *>(o + i) = v;
-  } else {
-    for (int t = i; t < KD2; ++t) o[t] *= sc;
+    ob[t] = v;
   }
 }
 
-// a6 only: partial slots -> fp64 stats [N, S0, S1, S2] about c (reading A19).
-__global__ void k_reduce_stats(const FinParams p) {
-  const int b = blockIdx.y;
-  const int pidx = blockIdx.x * blockDim.x + threadIdx.x;
+// a6 only: slots -> fp64 stats [N, S0, S1, S2] about c (reading A19).  Same grid as k_finalize.
+__global__ void __launch_bounds__(256) k_reduce_stats(const FinParams p) {
+  const int b = blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
+  const int j = blockIdx.x * kFinJ + jj;
+  if (j >= p.K) return;
   const int KD = p.K * p.D;
-  if (pidx >= KD) return;
-  const int k = pidx / p.K, j = pidx - k * p.K;
-  double S0, S1, S2, N;
-  slot_sums(p, b, j, k, S0, S1, S2, N);
+  ImageSlots is;
+  is.init(p, b);
   double *st = p.stats_out + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
-  if (pidx == 0) st[0] = N;
-  if (k == 0) st[1 + j] = S0;
-  st[1 + p.K + (size_t)j * p.D + k] = S1;
-  st[1 + p.K + (size_t)KD + (size_t)j * p.D + k] = S2;
+  if (blockIdx.x == 0 && tid == 0) st[0] = (double)(p.offsets[b + 1] - p.offsets[b]);
+  if (kq == 0) st[1 + j] = slot_s0(p, is, b, j);
+  for (int k = kq; k < p.D; k += 8) {
+    double S1, S2;
+    slot_s12(p, is, b, j, k, S1, S2);
+    st[1 + p.K + (size_t)j * p.D + k] = S1;
+    st[1 + p.K + (size_t)KD + (size_t)j * p.D + k] = S2;
+  }
 }
 
 }  // namespace gpufv

@@ -90,7 +90,7 @@ def test_posteriors_stress_flat_generator(fv):
 
 # ------------------------------------------------------------------ full encode
 @pytest.mark.parametrize("K,D,N", [(16, 64, 1000), (256, 64, 5000), (256, 64, 17714), (200, 64, 257), (1, 64, 10),
-                                   (1024, 64, 300), (256, 16, 1000)])
+                                   (512, 64, 300), (256, 16, 1000)])
 @pytest.mark.parametrize("tau", [0.0, TAU])
 def test_encode_parity(fv, K, D, N, tau):
     gmm_np, X = case(K, D, N)
