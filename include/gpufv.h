@@ -119,6 +119,10 @@ fv_status fv_posteriors(const float *X, int64_t N, int D, const float *weights, 
  * events on the stream it runs on.  Pass NULL, NULL to disable.  (cudaEvent_t values.) */
 void fv_profile_events(void *start_event, void *stop_event);
 
+/* Debug hook: in libraries built with -DGPUFV_TRACE, CTA 0 of k_stats records per-tile phase clocks
+ * (clock64) into dev_buf[64 x 16] (device memory, caller-owned); NULL disables.  No-op otherwise. */
+void fv_debug_trace(long long *dev_buf);
+
 /* Number of kernel launches the last successful call on this thread enqueued (for bench accounting). */
 int fv_last_launch_count(void);
 

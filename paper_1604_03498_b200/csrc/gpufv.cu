@@ -24,6 +24,7 @@ namespace {
 thread_local std::string g_err;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
+thread_local long long *g_trace = nullptr;
 
 fv_status fail(fv_status s, const char *fmt, ...) {
   char buf[512];
@@ -53,7 +54,9 @@ int num_clusters(int C) {
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
   std::lock_guard<std::mutex> lk(mu);
   if (cache[dev][C] > 0) return cache[dev][C];
-  if (cudaFuncSetAttribute(k_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(k_stats<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess)
+    return -1;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -66,7 +69,7 @@ int num_clusters(int C) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_stats, &cfg) != cudaSuccess || n <= 0) {
+  if (cudaOccupancyMaxActiveClusters(&n, k_stats<true>, &cfg) != cudaSuccess || n <= 0) {
     cudaGetLastError();
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -181,6 +184,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.slots = (float *)at(ws, L.slots);
   p.s0slots = (float *)at(ws, L.s0slots);
   p.gamma_out = gamma;
+  p.trace = g_trace;
   p.batch = batch;
   p.D = D;
   p.K = K;
@@ -221,12 +225,12 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (g_prof_start) cudaEventRecord(g_prof_start, st);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_stats, tmap, p);
+  cudaError_t e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false>, tmap, p);
   if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
   g_launches += 1;
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_stats);
+    cudaFuncGetAttributes(&fa, k_stats<true>);
     cudaGetLastError();
     return fail(FV_ERR_CUDA,
                 "k_stats launch: %s (grid %d x %d threads, cluster %d, dyn smem %d; kernel: %d regs, max threads %d, "
@@ -287,6 +291,7 @@ fv_status check_common(const float *X, int64_t n_total, int batch, int D, int K,
                        const float *mu, const float *sg, unsigned flags) {
   if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags)) return s;
   if (n_total < 0 || batch < 0) return fail(FV_ERR_ARG, "n_total=%lld, batch=%d must be >= 0", (long long)n_total, batch);
+  if (n_total >= (int64_t)1 << 31 - 1) return fail(FV_ERR_UNSUPPORTED, "n_total=%lld >= 2^30 per call (split the batch)", (long long)n_total);
   if (n_total > 0 && !X) return fail(FV_ERR_ARG, "null X");
   if (X && reinterpret_cast<uintptr_t>(X) % 16) return fail(FV_ERR_UNSUPPORTED, "X must be 16-byte aligned");
   if (std::isnan(thr) || thr >= 1.f) return fail(FV_ERR_ARG, "threshold must be < 1 and not NaN");
@@ -437,6 +442,8 @@ fv_status fv_posteriors(const float *X, int64_t N, int D, const float *w, const 
 }
 
 int fv_last_launch_count(void) { return g_launches; }
+
+void fv_debug_trace(long long *dev_buf) { g_trace = dev_buf; }
 
 void fv_profile_events(void *start_event, void *stop_event) {
   g_prof_start = static_cast<cudaEvent_t>(start_event);
