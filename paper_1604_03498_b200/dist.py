@@ -1,0 +1,104 @@
+"""Multi-GPU partitioning of the FV hot path (one process per GPU, torch.distributed).
+
+Two strategies:
+
+* Image/frame sharding (C3 batches, C4 streams): images are independent, so each rank encodes its own
+  share and there is no collective on the data path.  `shard_ranges` gives contiguous frame blocks;
+  `partition_images` balances ragged images (longest-processing-time greedy, deterministic).
+* Descriptor sharding (C5: one huge set): each rank computes the fp64 sufficient statistics
+  [N, S0, S1, S2] of its contiguous descriptor shard (`fv_stats_batched`), the statistics are summed
+  with one `all_reduce` (NCCL over NVLink on B200; they add exactly because they are sums over
+  descriptors — reading A19), and every rank runs `fv_finalize`.  `deterministic=True` replaces the
+  all-reduce by an all-gather and a fixed-order sum (bitwise repeatable across runs).
+
+The compute steps are injectable (`stats_fn`, `finalize_fn`, `encode_fn`) so the orchestration can be
+tested with world_size 2 on CPU over gloo; by default they are the CUDA library's entry points.
+"""
+from __future__ import annotations
+
+import heapq
+
+import torch
+import torch.distributed as dist
+
+
+def shard_ranges(n: int, world: int):
+    """Contiguous [lo, hi) ranges of n items over `world` ranks (sizes differ by at most 1)."""
+    return [(r * n // world, (r + 1) * n // world) for r in range(world)]
+
+
+def partition_images(counts, world: int):
+    """Longest-processing-time greedy assignment of images (by descriptor count) to ranks.
+    Returns one ascending index list per rank; ties broken by image index (deterministic)."""
+    heap = [(0, r) for r in range(world)]
+    parts = [[] for _ in range(world)]
+    for b in sorted(range(len(counts)), key=lambda i: (-int(counts[i]), i)):
+        load, r = heapq.heappop(heap)
+        parts[r].append(b)
+        heapq.heappush(heap, (load + int(counts[b]), r))
+    return [sorted(p) for p in parts]
+
+
+def _rank_world(group):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def encode_frames_sharded(X, offsets, gmm, threshold: float = 0.0, mode: int = 0, group=None, encode_fn=None,
+                          gather: bool = False):
+    """Frame-sharded encode: rank r encodes frames shard_ranges(B, world)[r].  X / offsets describe the
+    whole stream (offsets on the host); only this rank's rows are touched.  Returns this rank's FVs,
+    or all FVs in frame order when gather=True (an all_gather outside the hot path)."""
+    import numpy as np
+
+    rank, world = _rank_world(group)
+    off = np.asarray(offsets, dtype=np.int64)
+    B = off.shape[0] - 1
+    lo, hi = shard_ranges(B, world)[rank]
+    r0, r1 = int(off[lo]), int(off[hi])
+    local_off = torch.from_numpy(off[lo:hi + 1] - r0)
+    if encode_fn is None:
+        from . import encode_batched as _enc
+
+        def encode_fn(Xs, offs):
+            return _enc(Xs, offs.to(Xs.device), gmm, threshold=threshold, mode=mode)
+    out = encode_fn(X[r0:r1], local_off)
+    if not gather or world == 1:
+        return out
+    sizes = [b - a for a, b in shard_ranges(B, world)]
+    mx = max(sizes)  # all_gather needs equal shapes: pad to the largest shard, trim after
+    padded = out.new_zeros((mx, out.shape[1]))
+    padded[:out.shape[0]] = out
+    buf = [out.new_zeros((mx, out.shape[1])) for _ in sizes]
+    dist.all_gather(buf, padded, group=group)
+    return torch.cat([t[:s] for t, s in zip(buf, sizes)], 0)
+
+
+def encode_descriptor_sharded(X_shard, gmm, threshold: float = 0.0, mode: int = 0, group=None, stats_fn=None,
+                              finalize_fn=None, deterministic: bool = False):
+    """One descriptor set sharded over ranks: X_shard is this rank's contiguous rows.  Returns the
+    (identical on every rank) normalised FV of the whole set, shape (2KD,)."""
+    rank, world = _rank_world(group)
+    if stats_fn is None:
+        from . import stats_batched as _stats
+
+        def stats_fn(Xs):
+            offs = torch.tensor([0, Xs.shape[0]], dtype=torch.int64, device=Xs.device)
+            return _stats(Xs, offs, gmm, threshold=threshold)
+    if finalize_fn is None:
+        from . import finalize as _fin
+
+        def finalize_fn(st):
+            return _fin(st, gmm, mode=mode)
+    st = stats_fn(X_shard).reshape(1, -1).to(torch.float64)  # [N, S0, S1, S2] (a6)
+    if world > 1:
+        if deterministic:
+            parts = [torch.empty_like(st) for _ in range(world)]
+            dist.all_gather(parts, st, group=group)
+            st = parts[0].clone()
+            for t in parts[1:]:
+                st += t  # fixed rank order
+        else:
+            dist.all_reduce(st, op=dist.ReduceOp.SUM, group=group)  # a8
+    return finalize_fn(st).reshape(-1)

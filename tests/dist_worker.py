@@ -1,0 +1,40 @@
+"""Worker for tests/test_dist.py: one gloo rank (RANK/WORLD_SIZE/MASTER_* from the environment).
+Runs the dist orchestration with oracle-injected compute steps and saves results to $OUT_DIR."""
+import importlib.util
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import fvgen  # noqa: E402
+import oracle  # noqa: E402
+
+spec = importlib.util.spec_from_file_location("fvdist", os.path.join(ROOT, "paper_1604_03498_b200", "dist.py"))
+fvd = importlib.util.module_from_spec(spec)
+spec.loader.exec_module(fvd)
+
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+gmm = fvgen.make_gmm(16, 8, seed=31)
+X = fvgen.make_descriptors(gmm, 2001, seed=32)
+lo, hi = fvd.shard_ranges(X.shape[0], world)[rank]
+res = {}
+for det in (False, True):
+    fv = fvd.encode_descriptor_sharded(
+        X[lo:hi], gmm, threshold=1e-6,
+        stats_fn=lambda Xs: torch.from_numpy(oracle.stats(Xs, *gmm, threshold=1e-6)),
+        finalize_fn=lambda st: torch.from_numpy(oracle.fv_from_stats(st.numpy()[0], *gmm)),
+        deterministic=det)
+    res[f"desc_{det}"] = fv.numpy()
+Xb, off = fvgen.make_batch(gmm, [10, 300, 0, 77, 5], seed_base=33)
+out = fvd.encode_frames_sharded(
+    Xb, off, gmm, encode_fn=lambda Xs, o: torch.from_numpy(oracle.encode_batched(Xs, o.numpy(), *gmm, threshold=1e-6)),
+    gather=True)
+res["frames"] = out.numpy()
+np.savez(os.path.join(os.environ["OUT_DIR"], f"rank{rank}.npz"), **res)
+dist.destroy_process_group()

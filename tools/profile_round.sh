@@ -1,0 +1,15 @@
+#!/usr/bin/env bash
+# Run on the GPU box (gpurun): launch list of the bench command + one ncu --set full capture of
+# k_stats on the full C4 workload.  Outputs land in gpurun_out/ (scratch); tools/ncu_summary.py
+# turns them into the committed profiles/ summaries.
+set -u
+TAG=${1:-r01}
+python __graft_entry__.py
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/${TAG}_gpu.txt
+timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv \
+  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --e2e-steps 0 --no-latency --cpu-seconds 0 \
+  > gpurun_out/${TAG}_launches.log 2>&1
+timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k regex:k_stats -s 3 -c 1 \
+  -o gpurun_out/${TAG}_kstats python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-latency --cpu-seconds 0 \
+  > gpurun_out/${TAG}_kstats.log 2>&1
+tail -2 gpurun_out/${TAG}_kstats.log
