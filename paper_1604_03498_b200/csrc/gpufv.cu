@@ -82,7 +82,7 @@ int num_clusters(int C) {
 struct Layout {
   int C, Kp, ncl;
   int64_t n_total, nslots;                                         // fold slots (append-only S' chunks)
-  size_t wimg, bias, xshift, xscale, cshift, bscratch;  // prepared GMM (head of ws)
+  size_t wimg, bias, xshift, xscale, cshift, bscratch, coef;  // prepared GMM (head of ws)
   size_t tiles, off1, norm2, s0slots, slots;              // per call
   size_t hx, hoff, hout;                                  // _host entry point
   size_t total;
@@ -105,6 +105,7 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.xscale = o;   o = align_up(o + kDP * 4, 256);
   L.cshift = o;   o = align_up(o + kDP * 8, 256);
   L.bscratch = o; o = align_up(o + (size_t)L.Kp * 8, 1024);
+  L.coef = o;     o = align_up(o + (size_t)3 * kDP * L.Kp * 8, 1024);
   L.tiles = o;    o = align_up(o + (size_t)(batch + 1) * 8, 256);
   L.off1 = o;     o = align_up(o + 16, 256);
   L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 12, 1024);  // double norm2[] + uint counters[]
@@ -160,7 +161,7 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
   k_prep_shift<<<1, 256, 0, st>>>(w, mu, sg, K, D, L.Kp, sd, (double *)at(ws, L.cshift), (float *)at(ws, L.xshift),
                                   (float *)at(ws, L.xscale), (float *)at(ws, L.bias), (double *)at(ws, L.bscratch));
   k_prep_w<<<L.Kp, kNF, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
-                                 at(ws, L.wimg));
+                                 at(ws, L.wimg), (double *)at(ws, L.coef));
   g_launches += 2;
   return cuda_check("k_prep");
 }
@@ -243,21 +244,21 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
 
 FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, int D, const float *w, const float *mu,
                      const float *sg, unsigned flags, void *ws) {
+  (void)mu; (void)sg;
   FinParams f;
   f.slots = (const float *)at(ws, L.slots);
   f.s0slots = (const float *)at(ws, L.s0slots);
   f.stats = nullptr;
   f.offsets = offsets;
   f.tile_start = (const int64_t *)at(ws, L.tiles);
-  f.w = w; f.mu = mu; f.sg = sg;
-  f.cshift = (const double *)at(ws, L.cshift);
+  f.w = w;
+  f.coef = (const double *)at(ws, L.coef);
   f.xscale = (const float *)at(ws, L.xscale);
   f.out = nullptr;
   f.stats_out = nullptr;
   f.norm2 = (double *)at(ws, L.norm2);
   f.counters = (unsigned *)(f.norm2 + (batch > 0 ? batch : 1));
   f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
-  f.stddev = (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0;
   f.mode = (int)(flags & FV_NORM_MASK);
   return f;
 }
@@ -291,7 +292,7 @@ fv_status check_common(const float *X, int64_t n_total, int batch, int D, int K,
                        const float *mu, const float *sg, unsigned flags) {
   if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags)) return s;
   if (n_total < 0 || batch < 0) return fail(FV_ERR_ARG, "n_total=%lld, batch=%d must be >= 0", (long long)n_total, batch);
-  if (n_total >= (int64_t)1 << 31 - 1) return fail(FV_ERR_UNSUPPORTED, "n_total=%lld >= 2^30 per call (split the batch)", (long long)n_total);
+  if (n_total >= ((int64_t)1 << 30)) return fail(FV_ERR_UNSUPPORTED, "n_total=%lld >= 2^30 per call (split the batch)", (long long)n_total);
   if (n_total > 0 && !X) return fail(FV_ERR_ARG, "null X");
   if (X && reinterpret_cast<uintptr_t>(X) % 16) return fail(FV_ERR_UNSUPPORTED, "X must be 16-byte aligned");
   if (std::isnan(thr) || thr >= 1.f) return fail(FV_ERR_ARG, "threshold must be < 1 and not NaN");

@@ -80,16 +80,30 @@ __global__ void k_prep_shift(const float *w, const float *mu, const float *sg, i
 //   f <  64:  W'_jk      =  log2e (mu_jk - c_k) / var_jk * 2^-e_k
 //   f >= 64:  W'_j,64+k  = -log2e / (2 var_jk)          * 2^-2e_k
 // grid = Kp blocks (one Gaussian each), 128 threads (one feature each).
+//
+// Also writes the finalize coefficients coef[3][kDP][Kp] (a7, Eq. (6)-(7) of P:141-152 expanded about c):
+//   coef[0][k][j] = mu_jk - c_k,  coef[1][k][j] = 1 / sqrt(var_jk),  coef[2][k][j] = 1 / var_jk
+// (Gaussian-fastest so the finalize reads them coalesced; zero for padded j / k).
 __global__ void k_prep_w(const float *mu, const float *sg, int K, int D, int stddev, const double *cshift,
-                         const float *xscale, uint8_t *wimg) {
-  const int j = blockIdx.x, f = threadIdx.x;
+                         const float *xscale, uint8_t *wimg, double *coef) {
+  const int j = blockIdx.x, f = threadIdx.x, Kp = gridDim.x;
   const int k = f & (kDP - 1);
   double wv = 0.0;
   if (j < K && k < D) {
     const double v = gmm_var(sg, (size_t)j * D + k, stddev);
     const double s = (double)xscale[k];
-    if (f < kDP) wv = kLog2e * ((double)mu[(size_t)j * D + k] - cshift[k]) / v / s;
+    const double mup = (double)mu[(size_t)j * D + k] - cshift[k];
+    if (f < kDP) wv = kLog2e * mup / v / s;
     else wv = -kLog2e / (2.0 * v) / (s * s);
+    if (f < kDP) {
+      coef[(size_t)k * Kp + j] = mup;
+      coef[(size_t)(kDP + k) * Kp + j] = 1.0 / sqrt(v);
+      coef[(size_t)(2 * kDP + k) * Kp + j] = 1.0 / v;
+    }
+  } else if (f < kDP) {
+    coef[(size_t)k * Kp + j] = 0.0;
+    coef[(size_t)(kDP + k) * Kp + j] = 0.0;
+    coef[(size_t)(2 * kDP + k) * Kp + j] = 0.0;
   }
   const float w32 = (float)wv;
   const __half hi = __float2half_rn(w32);
@@ -148,114 +162,142 @@ struct FinParams {
   const double *stats;        // batch x (1 + K(2D+1)) (nullptr when reading slots)
   const int64_t *offsets;     // batch + 1 (slots mode)
   const int64_t *tile_start;  // batch + 1 (slots mode)
-  const float *w, *mu, *sg;
-  const double *cshift;
+  const float *w;
+  const double *coef;         // 3 x kDP x Kp (k_prep_w)
   const float *xscale;
   float *out;                 // batch x 2KD
   double *stats_out;          // k_reduce_stats output
   double *norm2;              // batch (zeroed before k_finalize)
   unsigned *counters;         // batch (zeroed before k_finalize): last-block ticket
-  int batch, K, Kp, D, ncl, stddev, mode;
+  int batch, K, Kp, D, ncl, mode;
 };
 
 // Owner cluster of global tile t under the static split [c T / ncl, (c+1) T / ncl).
 __device__ __forceinline__ int64_t tile_owner(int64_t t, int64_t T, int64_t ncl) { return ((t + 1) * ncl - 1) / T; }
 
-// The (cluster, segment) pieces of image b, in ascending cluster order (a6, fixed-order reduction).
-struct ImageSlots {
-  int64_t T, ft, lt, clo, chi;
-  __device__ void init(const FinParams &p, int b) {
-    T = p.tile_start[p.batch];
-    ft = p.tile_start[b];
-    lt = p.tile_start[b + 1];  // exclusive
-    clo = 0; chi = -1;
-    if (ft < lt) { clo = tile_owner(ft, T, p.ncl); chi = tile_owner(lt - 1, T, p.ncl); }
-  }
-  // segment of cluster c inside image b: [s0, s1) (empty if the cluster owns no tile)
-  __device__ void seg(const FinParams &p, int64_t c, int64_t &s0, int64_t &s1) const {
-    const int64_t st = c * T / p.ncl, en = (c + 1) * T / p.ncl;
-    s0 = st > ft ? st : ft;
-    s1 = en < lt ? en : lt;
-  }
-};
+constexpr int kFinJ = 32;       // Gaussians per finalize block
+constexpr int kFinKI = kDP / 8; // dims per thread: k = kq + 8 i
+constexpr int kMaxSeg = 160;    // clusters one image can span (ncl <= SM count)
 
-// S0_j (gamma units) and S1_jk, S2_jk (about c, unscaled) of image b: fixed-order fp64 sums.
-__device__ __forceinline__ double slot_s0(const FinParams &p, const ImageSlots &is, int b, int j) {
-  double S0 = 0.0;
-  for (int64_t c = is.clo; c <= is.chi; ++c) {
-    int64_t s0, s1;
-    is.seg(p, c, s0, s1);
-    if (s0 >= s1) continue;
-    S0 += (double)p.s0slots[(size_t)(c + b) * p.Kp + j];
-  }
-  return S0 / (double)kPScale;  // S0 was accumulated from P = gamma 2^14
-}
-__device__ __forceinline__ void slot_s12(const FinParams &p, const ImageSlots &is, int b, int j, int k, double &S1,
-                                         double &S2) {
-  S1 = S2 = 0.0;
-  for (int64_t c = is.clo; c <= is.chi; ++c) {
-    int64_t s0, s1;
-    is.seg(p, c, s0, s1);
-    for (int64_t tc = s0; tc < s1; tc += kFold) {
-      const float *sl = p.slots + (size_t)fold_slot(tc, c, b) * kNF * p.Kp;
-      S1 += (double)sl[(size_t)k * p.Kp + j];
-      S2 += (double)sl[(size_t)(kDP + k) * p.Kp + j];
+// The (cluster, tile range) segments of image b, in ascending cluster order, computed once per block
+// by thread 0 (a6: the fixed-order reduction of the per-cluster pieces).
+struct SegTable {
+  int n;
+  int c[kMaxSeg], s0[kMaxSeg], s1[kMaxSeg];
+};
+__device__ __forceinline__ void seg_table(const FinParams &p, int b, SegTable &t) {
+  const int64_t T = p.tile_start[p.batch], ft = p.tile_start[b], lt = p.tile_start[b + 1];
+  int n = 0;
+  if (ft < lt) {
+    const int64_t clo = tile_owner(ft, T, p.ncl), chi = tile_owner(lt - 1, T, p.ncl);
+    for (int64_t c = clo; c <= chi && n < kMaxSeg; ++c) {
+      const int64_t st = c * T / p.ncl, en = (c + 1) * T / p.ncl;
+      const int64_t a = st > ft ? st : ft, e = en < lt ? en : lt;
+      if (a >= e) continue;
+      t.c[n] = (int)c; t.s0[n] = (int)a; t.s1[n] = (int)e; ++n;
     }
   }
-  const double xs = (double)p.xscale[k];  // S1/S2 carry gamma 2^14 and the feature scales 2^e_k
-  S1 /= (double)kPScale * xs;
-  S2 /= (double)kPScale * xs * xs;
+  t.n = n;
 }
 
-constexpr int kFinJ = 32;  // Gaussians per finalize block
+// S0_j (gamma units) and S1_jk, S2_jk (about c, unscaled; k = kq + 8 i) of image b from the slots.
+__device__ __forceinline__ void slot_sums(const FinParams &p, const SegTable &t, int b, int j, int kq, double &S0,
+                                          double (&S1)[kFinKI], double (&S2)[kFinKI]) {
+  S0 = 0.0;
+#pragma unroll
+  for (int i = 0; i < kFinKI; ++i) S1[i] = S2[i] = 0.0;
+  for (int g = 0; g < t.n; ++g) {
+    const int c = t.c[g];
+    S0 += (double)p.s0slots[(size_t)(c + b) * p.Kp + j];
+    for (int tc = t.s0[g]; tc < t.s1[g]; tc += kFold) {
+      const float *sl = p.slots + (size_t)fold_slot(tc, c, b) * kNF * p.Kp + j;
+#pragma unroll
+      for (int i = 0; i < kFinKI; ++i) {
+        const int k = kq + 8 * i;
+        if (k < p.D) {
+          S1[i] += (double)sl[(size_t)k * p.Kp];
+          S2[i] += (double)sl[(size_t)(kDP + k) * p.Kp];
+        }
+      }
+    }
+  }
+  S0 *= 1.0 / (double)kPScale;  // S0 was accumulated from P = gamma 2^14
+#pragma unroll
+  for (int i = 0; i < kFinKI; ++i) {
+    const int k = kq + 8 * i;
+    if (k < p.D) {
+      const double xs = 1.0 / ((double)kPScale * (double)p.xscale[k]);  // powers of two: exact
+      S1[i] *= xs;
+      S2[i] *= xs * xs * (double)kPScale;  // S2 carries 2^14 once and the feature scale twice
+    }
+  }
+}
 
-// grid (ceil(K/32), batch), 256 threads.  Thread (jj = tid % 32, k = tid / 32 + 8 i): slot reads are
-// coalesced over jj; U/V go through a shared-memory tile so the global stores are coalesced over
-// (j, k).  Improved-FV scaling + signed sqrt in fp64; the L2 norm is accumulated with one atomic per
-// block and the LAST block of each image (ticket) rescales that image (its lines are still in L2).
+// grid (ceil(K/32), batch), 256 threads.  Thread (jj = tid % 32, kq = tid / 32) owns Gaussian
+// j0 + jj and dims kq + 8 i: slot and coefficient reads are coalesced over jj; U/V go through a
+// shared-memory tile so the global stores are coalesced over (j, k).  The Eq. (6)-(7) combination
+// runs in fp64; the signed square root (reading A9) in fp32 on the rounded value.  The L2 norm
+// is accumulated with one atomic per block and the LAST block of each image (ticket) rescales it.
 __global__ void __launch_bounds__(256) k_finalize(const FinParams p) {
   __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
+  __shared__ SegTable s_seg;
   __shared__ double s_red[8];
   __shared__ int s_last;
   const int b = blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
   const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), j = j0 + jj;
   const int KD = p.K * p.D;
+  if (p.slots && tid == 0) seg_table(p, b, s_seg);
+  __syncthreads();
   double ss = 0.0;
   if (jj < nj) {
-    double N, S0;
-    ImageSlots is;
-    const double *st = nullptr;
+    double N, S0, S1[kFinKI], S2[kFinKI];
     if (p.slots) {
       N = (double)(p.offsets[b + 1] - p.offsets[b]);
-      is.init(p, b);
-      S0 = slot_s0(p, is, b, j);
+      slot_sums(p, s_seg, b, j, kq, S0, S1, S2);
     } else {
-      st = p.stats + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
+      const double *st = p.stats + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
       N = st[0];
       S0 = st[1 + j];
+#pragma unroll
+      for (int i = 0; i < kFinKI; ++i) {
+        const int k = kq + 8 * i;
+        S1[i] = S2[i] = 0.0;
+        if (k < p.D) {
+          S1[i] = st[1 + p.K + (size_t)j * p.D + k];
+          S2[i] = st[1 + p.K + (size_t)KD + (size_t)j * p.D + k];
+        }
+      }
     }
-    const double pj = (double)p.w[j];
-    for (int k = kq; k < p.D; k += 8) {
-      double S1, S2;
-      if (p.slots) {
-        slot_s12(p, is, b, j, k, S1, S2);
-      } else {
-        S1 = st[1 + p.K + (size_t)j * p.D + k];
-        S2 = st[1 + p.K + (size_t)KD + (size_t)j * p.D + k];
+    double fu = 1.0, fv = 1.0;
+    if (p.mode == 0 && N > 0.0) {
+      const double pj = (double)p.w[j];
+      fu = 1.0 / (N * sqrt(pj));
+      fv = 1.0 / (N * sqrt(2.0 * pj));
+    }
+    const bool zero = (p.mode != 2) && !(N > 0.0);
+#pragma unroll
+    for (int i = 0; i < kFinKI; ++i) {
+      const int k = kq + 8 * i;
+      if (k < p.D) {
+        const double mup = p.coef[(size_t)k * p.Kp + j];
+        const double isd = p.coef[(size_t)(kDP + k) * p.Kp + j];
+        const double ivar = p.coef[(size_t)(2 * kDP + k) * p.Kp + j];
+        double U = (S1[i] - mup * S0) * isd;                                 // sum gamma (x - mu)/sd
+        double V = (S2[i] - 2.0 * mup * S1[i] + mup * mup * S0) * ivar - S0;  // sum gamma ((x-mu)^2/var - 1)
+        float u, v;
+        if (p.mode != 2) {
+          U = zero ? 0.0 : U * fu;
+          V = zero ? 0.0 : V * fv;
+          ss += fabs(U) + fabs(V);  // = (signed sqrt)^2
+          u = copysignf(sqrtf(fabsf((float)U)), (float)U);
+          v = copysignf(sqrtf(fabsf((float)V)), (float)V);
+        } else {
+          u = (float)U;
+          v = (float)V;
+        }
+        sU[jj][k] = u;
+        sV[jj][k] = v;
       }
-      const double var = gmm_var(p.sg, (size_t)j * p.D + k, p.stddev);
-      const double mup = (double)p.mu[(size_t)j * p.D + k] - p.cshift[k];
-      double U = (S1 - mup * S0) / sqrt(var);                         // sum gamma (x - mu)/sd
-      double V = (S2 - 2.0 * mup * S1 + mup * mup * S0) / var - S0;  // sum gamma ((x-mu)^2/var - 1)
-      if (p.mode != 2) {
-        if (N <= 0.0) { U = 0.0; V = 0.0; }
-        if (p.mode == 0) { U /= N * sqrt(pj); V /= N * sqrt(2.0 * pj); }
-        ss += fabs(U) + fabs(V);  // = (signed sqrt)^2
-        U = (U > 0.0) ? sqrt(U) : ((U < 0.0) ? -sqrt(-U) : 0.0);
-        V = (V > 0.0) ? sqrt(V) : ((V < 0.0) ? -sqrt(-V) : 0.0);
-      }
-      sU[jj][k] = (float)U;
-      sV[jj][k] = (float)V;
     }
   }
   __syncthreads();
@@ -294,20 +336,25 @@ __global__ void __launch_bounds__(256) k_finalize(const FinParams p) {
 
 // a6 only: slots -> fp64 stats [N, S0, S1, S2] about c (reading A19).  Same grid as k_finalize.
 __global__ void __launch_bounds__(256) k_reduce_stats(const FinParams p) {
+  __shared__ SegTable s_seg;
   const int b = blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
   const int j = blockIdx.x * kFinJ + jj;
+  if (tid == 0) seg_table(p, b, s_seg);
+  __syncthreads();
   if (j >= p.K) return;
   const int KD = p.K * p.D;
-  ImageSlots is;
-  is.init(p, b);
+  double S0, S1[kFinKI], S2[kFinKI];
+  slot_sums(p, s_seg, b, j, kq, S0, S1, S2);
   double *st = p.stats_out + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
   if (blockIdx.x == 0 && tid == 0) st[0] = (double)(p.offsets[b + 1] - p.offsets[b]);
-  if (kq == 0) st[1 + j] = slot_s0(p, is, b, j);
-  for (int k = kq; k < p.D; k += 8) {
-    double S1, S2;
-    slot_s12(p, is, b, j, k, S1, S2);
-    st[1 + p.K + (size_t)j * p.D + k] = S1;
-    st[1 + p.K + (size_t)KD + (size_t)j * p.D + k] = S2;
+  if (kq == 0) st[1 + j] = S0;
+#pragma unroll
+  for (int i = 0; i < kFinKI; ++i) {
+    const int k = kq + 8 * i;
+    if (k < p.D) {
+      st[1 + p.K + (size_t)j * p.D + k] = S1[i];
+      st[1 + p.K + (size_t)KD + (size_t)j * p.D + k] = S2[i];
+    }
   }
 }
 

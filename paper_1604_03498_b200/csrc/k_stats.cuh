@@ -54,9 +54,9 @@ constexpr int kS2Z = kS2P + 2 * kOpBytes;            // Z hi | lo             64
 constexpr int kS2X = kS2Z + 2 * kOpBytes;            // X box stage           16 KB
 constexpr int kXBoxBytes = 128 * 128;                // 32 floats x 128 rows
 constexpr int kS2Bias = kS2X + kXBoxBytes;           // float[128]
-constexpr int kS2Cs = kS2Bias + kG * 4;              // float[64]  c_k 2^e_k
+constexpr int kS2Cs = kS2Bias + kG * 4;              // float[64]  -c_k 2^e_k
 constexpr int kS2Sc = kS2Cs + kDP * 4;               // float[64]  2^e_k
-constexpr int kS2Red = kS2Sc + kDP * 4;              // float[2][4][128] (max, sum) per column quarter
+constexpr int kS2Red = kS2Sc + kDP * 4;              // float2[4][128] (max, sum) per column quarter
 constexpr int kS2Xchg = kS2Red + 2 * 4 * kTileM * 4; // float2[2][kMaxC2][128]
 constexpr int kS2S0 = kS2Xchg + 2 * kMaxC2 * kTileM * 8;  // float[4][128]
 constexpr int kS2Meta = kS2S0 + 4 * kG * 4;          // TileMeta[4]
@@ -165,7 +165,7 @@ __device__ __forceinline__ void warp_transpose_reduce32(float (&a)[32], int lane
 // lo -> + 64.  kMask: dims >= D or a row past the image end are zeroed.
 template <bool kMask>
 __device__ __forceinline__ void zr_box(const uint8_t *xbox, int row, int box, int h, int D, bool valid,
-                                       const float *s_sc, const float *s_cs, uint32_t taddr) {
+                                       const float *s_sc, const float *s_ncs, uint32_t taddr) {
   using namespace ptx;
   uint32_t lh[4], ll[4], qh[4], ql[4];
   const int k0 = 32 * box + 8 * h;
@@ -173,16 +173,20 @@ __device__ __forceinline__ void zr_box(const uint8_t *xbox, int row, int box, in
   for (int c2 = 0; c2 < 2; ++c2) {
     const float4 v = *reinterpret_cast<const float4 *>(xbox + sw_off(row, 2 * h + c2));
     const float4 sc = *reinterpret_cast<const float4 *>(s_sc + k0 + 4 * c2);
-    const float4 cs = *reinterpret_cast<const float4 *>(s_cs + k0 + 4 * c2);
-    float a[4] = {fmaf(v.x, sc.x, -cs.x), fmaf(v.y, sc.y, -cs.y), fmaf(v.z, sc.z, -cs.z), fmaf(v.w, sc.w, -cs.w)};
+    const float4 ncs = *reinterpret_cast<const float4 *>(s_ncs + k0 + 4 * c2);
+    float2 a0 = __ffma2_rn(make_float2(v.x, v.y), make_float2(sc.x, sc.y), make_float2(ncs.x, ncs.y));
+    float2 a1 = __ffma2_rn(make_float2(v.z, v.w), make_float2(sc.z, sc.w), make_float2(ncs.z, ncs.w));
     if (kMask) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) if (!valid || k0 + 4 * c2 + e >= D) a[e] = 0.f;
+      const int kk = k0 + 4 * c2;
+      if (!valid || kk >= D) a0.x = 0.f;
+      if (!valid || kk + 1 >= D) a0.y = 0.f;
+      if (!valid || kk + 2 >= D) a1.x = 0.f;
+      if (!valid || kk + 3 >= D) a1.y = 0.f;
     }
-    split2_f16(a[0], a[1], lh[2 * c2], ll[2 * c2]);
-    split2_f16(a[2], a[3], lh[2 * c2 + 1], ll[2 * c2 + 1]);
-    split2_f16(a[0] * a[0], a[1] * a[1], qh[2 * c2], ql[2 * c2]);
-    split2_f16(a[2] * a[2], a[3] * a[3], qh[2 * c2 + 1], ql[2 * c2 + 1]);
+    split2_f16(a0, lh[2 * c2], ll[2 * c2]);
+    split2_f16(a1, lh[2 * c2 + 1], ll[2 * c2 + 1]);
+    split2_f16(__fmul2_rn(a0, a0), qh[2 * c2], ql[2 * c2]);
+    split2_f16(__fmul2_rn(a1, a1), qh[2 * c2 + 1], ql[2 * c2 + 1]);
   }
   tmem_st4(taddr + k0 / 2, lh);
   tmem_st4(taddr + 32 + k0 / 2, qh);
@@ -216,9 +220,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   uint8_t *smem = smem_raw + (sbase - raw_base);
   const uint32_t sW = sbase + kS2W, sP = sbase + kS2P, sZ = sbase + kS2Z, sX = sbase + kS2X;
   float *s_bias = reinterpret_cast<float *>(smem + kS2Bias);
-  float *s_cs = reinterpret_cast<float *>(smem + kS2Cs);
+  float *s_ncs = reinterpret_cast<float *>(smem + kS2Cs);
   float *s_sc = reinterpret_cast<float *>(smem + kS2Sc);
-  float *s_red = reinterpret_cast<float *>(smem + kS2Red);
+  float2 *s_red = reinterpret_cast<float2 *>(smem + kS2Red);
   float2 *s_xchg = reinterpret_cast<float2 *>(smem + kS2Xchg);
   float *s_s0 = reinterpret_cast<float *>(smem + kS2S0);
   TileMeta *s_meta = reinterpret_cast<TileMeta *>(smem + kS2Meta);
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     uint4 *dst = reinterpret_cast<uint4 *>(smem + kS2W);
     for (int i = tid; i < kWImgBytes / 16; i += kThreads2) dst[i] = __ldg(src + i);
     for (int i = tid; i < kG; i += kThreads2) s_bias[i] = p.bias[rank * kG + i];
-    if (tid < kDP) { s_sc[tid] = p.xscale[tid]; s_cs[tid] = p.xshift[tid] * p.xscale[tid]; }
+    if (tid < kDP) { s_sc[tid] = p.xscale[tid]; s_ncs[tid] = -(p.xshift[tid] * p.xscale[tid]); }
   }
   if (warp == 0) { tmem_alloc(s_tmem, kTmemCols); tmem_relinquish(); }
   if (tid == 0) {
@@ -349,18 +353,19 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     const int row = 32 * q + lane;  // descriptor row of Zr / L / P / Z; feature of S'
     const int D = kD64 ? kDP : p.D;
     const float thr = p.threshold * kPScale;
-    float *red_m = s_red, *red_s = s_red + 4 * kTileM;
     const uint8_t *xbox = smem + kS2X;
 
     // Zr(i), box `box`: this warp converts dims 32 box + 8h .. +8 of row `row`; all 16 WORK warps
-    // share each box, so a box is released after ~1/16 of the tile's conversion work
+    // share each box, so a box is released after ~1/16 of the tile's conversion work.  Box 0 needs no
+    // wait::st (its X values are consumed by the time the stores issue); box 1 waits for all of this
+    // thread's Zr(i) stores before ZR_FULL.
     auto conv_box = [&](int i, int box) {
       mbar_wait(&bars[B_XFULL0 + box], i & 1);
       const int nrows = s_meta[i & 3].nrows;
       const uint32_t ta = tmem + kTZr + 128 * (i & 1) + lane_base;
-      if (!kD64 || nrows < kTileM) zr_box<true>(xbox, row, box, h, D, row < nrows, s_sc, s_cs, ta);
-      else zr_box<false>(xbox, row, box, h, D, true, s_sc, s_cs, ta);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // also orders the X reads
+      if (!kD64 || nrows < kTileM) zr_box<true>(xbox, row, box, h, D, row < nrows, s_sc, s_ncs, ta);
+      else zr_box<false>(xbox, row, box, h, D, true, s_sc, s_ncs, ta);
+      if (box == 1) tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -370,27 +375,31 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     };
     auto copy_z = [&](int i) {  // this warp's Zr(i) words -> Z rows in shared memory (GEMM2 A operand)
       const uint32_t ta = tmem + kTZr + 128 * (i & 1) + lane_base;
+      uint32_t z[32];
 #pragma unroll
       for (int box = 0; box < 2; ++box) {
-        const int c = 4 * box + h;  // 16-byte chunk of the 64-feature atom holding dims 32 box + 8h ..
-        uint32_t lh[4], qh[4], ll[4], ql[4];
-        tmem_ld4(ta + 16 * box + 4 * h, lh);
-        tmem_ld4(ta + 32 + 16 * box + 4 * h, qh);
-        tmem_ld4(ta + 64 + 16 * box + 4 * h, ll);
-        tmem_ld4(ta + 96 + 16 * box + 4 * h, ql);
-        tmem_ld_wait();
-        const uint32_t o = sw_off(row, c);
-        sts128(sZ + o, lh[0], lh[1], lh[2], lh[3]);
-        sts128(sZ + kAtomBytes + o, qh[0], qh[1], qh[2], qh[3]);
-        sts128(sZ + kOpBytes + o, ll[0], ll[1], ll[2], ll[3]);
-        sts128(sZ + kOpBytes + kAtomBytes + o, ql[0], ql[1], ql[2], ql[3]);
+        uint32_t(&zb)[16] = *reinterpret_cast<uint32_t(*)[16]>(z + 16 * box);
+        tmem_ld4(ta + 16 * box + 4 * h, *reinterpret_cast<uint32_t(*)[4]>(zb + 0));        // lin hi
+        tmem_ld4(ta + 32 + 16 * box + 4 * h, *reinterpret_cast<uint32_t(*)[4]>(zb + 4));   // quad hi
+        tmem_ld4(ta + 64 + 16 * box + 4 * h, *reinterpret_cast<uint32_t(*)[4]>(zb + 8));   // lin lo
+        tmem_ld4(ta + 96 + 16 * box + 4 * h, *reinterpret_cast<uint32_t(*)[4]>(zb + 12));  // quad lo
+      }
+      tmem_ld_wait(z);
+#pragma unroll
+      for (int box = 0; box < 2; ++box) {
+        const uint32_t o = sw_off(row, 4 * box + h);  // 16-byte chunk of the atom holding dims 32 box + 8h ..
+        const uint32_t *zb = z + 16 * box;
+        sts128(sZ + o, zb[0], zb[1], zb[2], zb[3]);
+        sts128(sZ + kAtomBytes + o, zb[4], zb[5], zb[6], zb[7]);
+        sts128(sZ + kOpBytes + o, zb[8], zb[9], zb[10], zb[11]);
+        sts128(sZ + kOpBytes + kAtomBytes + o, zb[12], zb[13], zb[14], zb[15]);
       }
     };
     auto fold = [&](int b, int chunk_start) {  // S' quarter (lane = feature, columns 32h..) -> slot
       float *dst = p.slots + (size_t)fold_slot(chunk_start, cid, b) * kNF * p.Kp + (size_t)row * p.Kp + rank * kG + 32 * h;
       uint32_t v[32];
       tmem_ld32(tmem + kTS + lane_base + 32 * h, v);
-      tmem_ld_wait();
+      tmem_ld_wait(v);
       float4 *d4 = reinterpret_cast<float4 *>(dst);
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -408,16 +417,16 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       TRW(0);
       work_wait(&bars[B_G1_DONE], i & 1, warp);  // L(i) ready; Zr((i+1)%2) free (GEMM1(i-1) done)
       TRW(1);
-      if (i + 1 < n) conv_box(i + 1, 0);  // box 1 streams in behind the L load / row max below
-      TRW(2);
-      const TileMeta mt = s_meta[i & 3];
-
-      // ---- softmax(i): L row quarter -> e = 2^(L + b - m), row sum, cluster combine
+      // ---- softmax(i), online form: this warp's column quarter is exponentiated against its own row
+      // max m_h; the (m_h, s_h) pairs of the 4 quarters (one named barrier) and of the cluster's CTAs
+      // (DSMEM) are then combined into the row's (M, S) and each quarter rescaled by 2^(m_h - M) / S.
       float v[32];
       {
         uint32_t rr[32];
         tmem_ld32(tmem + kTL + lane_base + 32 * h, rr);
-        tmem_ld_wait();
+        if (i + 1 < n) conv_box(i + 1, 0);  // overlaps the TMEM load; box 1 streams in meanwhile
+        TRW(2);
+        tmem_ld_wait(rr);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
       }
@@ -425,32 +434,40 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_L_EMPTY]);
       TRW(3);
+      const TileMeta mt = s_meta[i & 3];
       float m = -3.0e38f;
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
         const float4 bj = *reinterpret_cast<const float4 *>(s_bias + 32 * h + j);
-        v[j] += bj.x; v[j + 1] += bj.y; v[j + 2] += bj.z; v[j + 3] += bj.w;
-        m = fmaxf(m, fmaxf(fmaxf(v[j], v[j + 1]), fmaxf(v[j + 2], v[j + 3])));
+        const float2 x0 = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(bj.x, bj.y));
+        const float2 x1 = __fadd2_rn(make_float2(v[j + 2], v[j + 3]), make_float2(bj.z, bj.w));
+        v[j] = x0.x; v[j + 1] = x0.y; v[j + 2] = x1.x; v[j + 3] = x1.y;
+        m = fmaxf(m, fmaxf(fmaxf(x0.x, x0.y), fmaxf(x1.x, x1.y)));
       }
       if (p.gamma_mode == 2 && row < mt.nrows) {
         float *go = p.gamma_out + (size_t)(mt.row0 + row) * p.K;
 #pragma unroll
         for (int j = 0; j < 32; ++j) { int gj = rank * kG + 32 * h + j; if (gj < p.K) go[gj] = v[j]; }
       }
-      red_m[h * kTileM + row] = m;
+      float2 sacc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float2 d = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(-m, -m));
+        v[j] = ex2_approx(d.x); v[j + 1] = ex2_approx(d.y);
+        sacc = __fadd2_rn(sacc, make_float2(v[j], v[j + 1]));
+      }
+      TRW(4);
+      s_red[h * kTileM + row] = make_float2(m, sacc.x + sacc.y);
       if (i + 1 < n) conv_box(i + 1, 1);
       named_bar_sync(kBarLane0 + q, 128);
-      TRW(4);
-      m = fmaxf(fmaxf(red_m[row], red_m[kTileM + row]), fmaxf(red_m[2 * kTileM + row], red_m[3 * kTileM + row]));
-      float s = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) { v[j] = ex2_approx(v[j] - m); s += v[j]; }
-      TRW(11);
-      red_s[h * kTileM + row] = s;
-      named_bar_sync(kBarLane0 + q, 128);
       TRW(5);
-      s = (red_s[row] + red_s[kTileM + row]) + (red_s[2 * kTileM + row] + red_s[3 * kTileM + row]);
-      float alpha;
+      float M, S;
+      {
+        const float2 r0 = s_red[row], r1 = s_red[kTileM + row], r2 = s_red[2 * kTileM + row], r3 = s_red[3 * kTileM + row];
+        M = fmaxf(fmaxf(r0.x, r1.x), fmaxf(r2.x, r3.x));
+        S = (r0.y * ex2_approx(r0.x - M) + r1.y * ex2_approx(r1.x - M)) +
+            (r2.y * ex2_approx(r2.x - M) + r3.y * ex2_approx(r3.x - M));
+      }
       if (C > 1) {
         const int par = i & 1;
         float2 *xb = s_xchg + par * (kMaxC2 * kTileM);
@@ -459,22 +476,27 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
           const uint32_t my = smem_u32(&xb[rank * kTileM + row]);
           const uint32_t mybar = smem_u32(&bars[B_XCHG0 + par]);
           for (uint32_t r2 = 0; r2 < C; ++r2)
-            if (r2 != rank) st_async_v2f32(mapa_shared(my, r2), m, s, mapa_shared(mybar, r2));
+            if (r2 != rank) st_async_v2f32(mapa_shared(my, r2), M, S, mapa_shared(mybar, r2));
         }
         TRW(13);
         mbar_wait(&bars[B_XCHG0 + par], (i >> 1) & 1);
         TRW(12);
-        float M = m;
-        for (uint32_t r2 = 0; r2 < C; ++r2) if (r2 != rank) M = fmaxf(M, xb[r2 * kTileM + row].x);
-        float S = s * ex2_approx(m - M);
-        for (uint32_t r2 = 0; r2 < C; ++r2)
-          if (r2 != rank) { const float2 o = xb[r2 * kTileM + row]; S += o.y * ex2_approx(o.x - M); }
-        alpha = __fdividef(ex2_approx(m - M), S);
-      } else {
-        alpha = __frcp_rn(s);
+        float2 o[kMaxC2];
+        float Mg = M;
+#pragma unroll
+        for (int r2 = 0; r2 < kMaxC2; ++r2) {
+          o[r2] = make_float2(-3.0e38f, 0.f);
+          if (r2 < (int)C && r2 != (int)rank) { o[r2] = xb[r2 * kTileM + row]; Mg = fmaxf(Mg, o[r2].x); }
+        }
+        float Sg = S * ex2_approx(M - Mg);
+#pragma unroll
+        for (int r2 = 0; r2 < kMaxC2; ++r2) Sg += o[r2].y * ex2_approx(o[r2].x - Mg);
+        M = Mg;
+        S = Sg;
       }
-      if (row >= mt.nrows) alpha = 0.f;
-      const float alpha_p = alpha * kPScale;  // P = gamma 2^14
+      // this quarter's gamma_ij = e_ij 2^(m_h - M) / S; P = gamma 2^14
+      float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
+      if (row >= mt.nrows) alpha_p = 0.f;
       TRW(6);
 
       // ---- GEMM2(i-1) done: S' chunk complete (fold), Z and P free
@@ -489,20 +511,21 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       }
       TRW(7);
       if (mt.flags & 2) chunk_start = mt.t;
-      copy_z(i);
-      TRW(8);
 
-      // ---- P(i) = gamma 2^14 (thresholded) -> fp16 hi/lo, S0 accumulation
+      // ---- P(i) = gamma 2^14 (thresholded: gamma <= tau -> 0) -> fp16 hi/lo, S0 accumulation
+      const float2 ap = make_float2(alpha_p, alpha_p);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
-          float g0 = v[8 * c + e] * alpha_p, g1 = v[8 * c + e + 1] * alpha_p;
-          if (thr > 0.f) { g0 = (g0 > thr) ? g0 : 0.f; g1 = (g1 > thr) ? g1 : 0.f; }
-          v[8 * c + e] = g0; v[8 * c + e + 1] = g1;
-          s0acc[8 * c + e] += g0; s0acc[8 * c + e + 1] += g1;
-          split2_f16(g0, g1, hi[e >> 1], lo[e >> 1]);
+          const int j = 8 * c + e;
+          float2 g = __fmul2_rn(make_float2(v[j], v[j + 1]), ap);
+          if (thr > 0.f) g = __fmul2_rn(g, make_float2(set_gt(g.x, thr), set_gt(g.y, thr)));
+          v[j] = g.x; v[j + 1] = g.y;
+          const float2 sa = __fadd2_rn(make_float2(s0acc[j], s0acc[j + 1]), g);
+          s0acc[j] = sa.x; s0acc[j + 1] = sa.y;
+          split2_f16(g, hi[e >> 1], lo[e >> 1]);
         }
         const uint32_t off = (h >> 1) * kAtomBytes + sw_off(row, 4 * (h & 1) + c);
         sts128(sP + off, hi[0], hi[1], hi[2], hi[3]);
@@ -513,6 +536,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
 #pragma unroll
         for (int j = 0; j < 32; ++j) { int gj = rank * kG + 32 * h + j; if (gj < p.K) go[gj] = v[j] * (1.f / kPScale); }
       }
+      TRW(8);
+      copy_z(i);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();

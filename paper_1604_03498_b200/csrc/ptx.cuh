@@ -124,6 +124,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait::ld, then re-define the destination registers of the outstanding loads so that no use of them
+// can be scheduled above the wait (the registers of tcgen05.ld are undefined until it completes).
+template <int N>
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[N]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i]));
+}
 
 // D[tmem] (+)= A[tmem] * B[smem] ("TS" form; A is K-major in TMEM: lane = row m, 32-bit column c holds
 // the fp16 pair (k = 2c, 2c + 1)).  disable-output-lane mask all zero.
@@ -234,6 +242,23 @@ __device__ __forceinline__ void split2_f16(float a, float b, uint32_t &hi, uint3
   __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
   hi = *reinterpret_cast<uint32_t *>(&h);
   lo = *reinterpret_cast<uint32_t *>(&l);
+}
+
+// Packed-pair variant (sm_100 FADD2): hi = fp16(a) RN, lo = fp16(a - hi) RN for both halves.
+__device__ __forceinline__ void split2_f16(float2 a, uint32_t &hi, uint32_t &lo) {
+  __half2 h = __floats2half2_rn(a.x, a.y);
+  const float2 hf = __half22float2(h);
+  const float2 d = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
+  __half2 l = __floats2half2_rn(d.x, d.y);
+  hi = *reinterpret_cast<uint32_t *>(&h);
+  lo = *reinterpret_cast<uint32_t *>(&l);
+}
+
+// 1.0f if a > b else 0.0f (FSET.BF)
+__device__ __forceinline__ float set_gt(float a, float b) {
+  float r;
+  asm("set.gt.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
 }
 
 __device__ __forceinline__ void sts128(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
