@@ -56,10 +56,9 @@ constexpr int kXBoxBytes = 128 * 128;                // 32 floats x 128 rows
 constexpr int kS2Bias = kS2X + kXBoxBytes;           // float[128]
 constexpr int kS2Cs = kS2Bias + kG * 4;              // float[64]  -c_k 2^e_k
 constexpr int kS2Sc = kS2Cs + kDP * 4;               // float[64]  2^e_k
-constexpr int kS2Red = kS2Sc + kDP * 4;              // float2[4][128] (max, sum) per column quarter
-constexpr int kS2Xchg = kS2Red + 2 * 4 * kTileM * 4; // float2[2][kMaxC2][128]
-constexpr int kS2S0 = kS2Xchg + 2 * kMaxC2 * kTileM * 8;  // float[4][128]
-constexpr int kS2Meta = kS2S0 + 4 * kG * 4;          // TileMeta[4]
+constexpr int kS2Red = kS2Sc + kDP * 4;              // float2[2][4][128] (max, sum) per column quarter, by tile parity
+constexpr int kS2Xchg = kS2Red + 2 * 4 * kTileM * 8; // float2[2][kMaxC2][128]
+constexpr int kS2Meta = kS2Xchg + 2 * kMaxC2 * kTileM * 8;  // TileMeta[4]
 constexpr int kS2Bar = kS2Meta + 128;                // uint64 barriers
 constexpr int kNumBars = 16;
 constexpr int kS2Tmem = kS2Bar + kNumBars * 8;
@@ -194,11 +193,11 @@ __device__ __forceinline__ void zr_box(const uint8_t *xbox, int row, int box, in
   tmem_st4(taddr + 96 + k0 / 2, ql);
 }
 
-// WORK-warp wait on an MMA-completion barrier: one elected warp polls, the others park on a named
-// barrier (no issue slots burnt by 16 pollers).
-__device__ __forceinline__ void work_wait(uint64_t *bar, uint32_t parity, int warp) {
-  if (warp == 0) ptx::mbar_wait(bar, parity);
-  ptx::named_bar_sync(kBarWork, kWarpsWork * 32);
+// WORK-warp wait on an MMA-completion barrier.  Every warp waits on its own (try_wait suspends the
+// warp instead of spinning), so the 16 warps are never coupled by a CTA-wide barrier here.  No warp
+// can lag two phases behind: G1(i+1) needs ZR_FULL(i+1) and G2(i) needs P_FULL(i) from all 16 warps.
+__device__ __forceinline__ void work_wait(uint64_t *bar, uint32_t parity) {
+  ptx::mbar_wait(bar, parity);
   ptx::tc_fence_after();
 }
 
@@ -224,7 +223,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   float *s_sc = reinterpret_cast<float *>(smem + kS2Sc);
   float2 *s_red = reinterpret_cast<float2 *>(smem + kS2Red);
   float2 *s_xchg = reinterpret_cast<float2 *>(smem + kS2Xchg);
-  float *s_s0 = reinterpret_cast<float *>(smem + kS2S0);
+  // S0 segment flush scratch float[4][128]: aliases the (m, s) buffer of the NEXT tile's parity, which
+  // no warp reads or writes between the two kBarWork barriers of the flush
+  float *s_s0_base = reinterpret_cast<float *>(smem + kS2Red);
   TileMeta *s_meta = reinterpret_cast<TileMeta *>(smem + kS2Meta);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kS2Bar);
   uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + kS2Tmem);
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     if (n > 0) { conv_box(0, 0); conv_box(0, 1); }
     for (int i = 0; i < n; ++i) {
       TRW(0);
-      work_wait(&bars[B_G1_DONE], i & 1, warp);  // L(i) ready; Zr((i+1)%2) free (GEMM1(i-1) done)
+      work_wait(&bars[B_G1_DONE], i & 1);  // L(i) ready; Zr((i+1)%2) free (GEMM1(i-1) done)
       TRW(1);
       // ---- softmax(i), online form: this warp's column quarter is exponentiated against its own row
       // max m_h; the (m_h, s_h) pairs of the 4 quarters (one named barrier) and of the cluster's CTAs
@@ -424,7 +425,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       {
         uint32_t rr[32];
         tmem_ld32(tmem + kTL + lane_base + 32 * h, rr);
-        if (i + 1 < n) conv_box(i + 1, 0);  // overlaps the TMEM load; box 1 streams in meanwhile
         TRW(2);
         tmem_ld_wait(rr);
 #pragma unroll
@@ -449,21 +449,37 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
 #pragma unroll
         for (int j = 0; j < 32; ++j) { int gj = rank * kG + 32 * h + j; if (gj < p.K) go[gj] = v[j]; }
       }
-      float2 sacc = make_float2(0.f, 0.f);
+      auto exp_local = [&]() {  // e = 2^(v - m_h) in place; returns the quarter's row sum s_h
+        float2 sacc = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float2 d = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(-m, -m));
-        v[j] = ex2_approx(d.x); v[j + 1] = ex2_approx(d.y);
-        sacc = __fadd2_rn(sacc, make_float2(v[j], v[j + 1]));
+        for (int j = 0; j < 32; j += 2) {
+          const float2 d = __fadd2_rn(make_float2(v[j], v[j + 1]), make_float2(-m, -m));
+          v[j] = ex2_approx(d.x); v[j + 1] = ex2_approx(d.y);
+          sacc = __fadd2_rn(sacc, make_float2(v[j], v[j + 1]));
+        }
+        return sacc.x + sacc.y;
+      };
+      float2 *red = s_red + (i & 1) * (4 * kTileM);  // parity buffer: tile i+1 never overwrites tile i's
+      if (i + 1 < n) {
+        // Zr(i+1) box 0 (resident since the previous tile) in the same basic block as the exp loop:
+        // its FMA/ALU work fills the issue slots the MUFU-bound exponentials leave idle
+        mbar_wait(&bars[B_XFULL0], (i + 1) & 1);
+        const int nr1 = s_meta[(i + 1) & 3].nrows;
+        const float ssum = exp_local();
+        zr_box<true>(xbox, row, 0, h, D, row < nr1, s_sc, s_ncs, tmem + kTZr + 128 * ((i + 1) & 1) + lane_base);
+        red[h * kTileM + row] = make_float2(m, ssum);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[B_XEMPTY0]);  // box 1 streams in behind the combine below
+      } else {
+        red[h * kTileM + row] = make_float2(m, exp_local());
       }
       TRW(4);
-      s_red[h * kTileM + row] = make_float2(m, sacc.x + sacc.y);
-      if (i + 1 < n) conv_box(i + 1, 1);
       named_bar_sync(kBarLane0 + q, 128);
       TRW(5);
       float M, S;
       {
-        const float2 r0 = s_red[row], r1 = s_red[kTileM + row], r2 = s_red[2 * kTileM + row], r3 = s_red[3 * kTileM + row];
+        const float2 r0 = red[row], r1 = red[kTileM + row], r2 = red[2 * kTileM + row], r3 = red[3 * kTileM + row];
         M = fmaxf(fmaxf(r0.x, r1.x), fmaxf(r2.x, r3.x));
         S = (r0.y * ex2_approx(r0.x - M) + r1.y * ex2_approx(r1.x - M)) +
             (r2.y * ex2_approx(r2.x - M) + r3.y * ex2_approx(r3.x - M));
@@ -479,6 +495,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
             if (r2 != rank) st_async_v2f32(mapa_shared(my, r2), M, S, mapa_shared(mybar, r2));
         }
         TRW(13);
+        if (i + 1 < n) conv_box(i + 1, 1);  // fills the partner-exchange latency
         mbar_wait(&bars[B_XCHG0 + par], (i >> 1) & 1);
         TRW(12);
         float2 o[kMaxC2];
@@ -493,6 +510,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         for (int r2 = 0; r2 < kMaxC2; ++r2) Sg += o[r2].y * ex2_approx(o[r2].x - Mg);
         M = Mg;
         S = Sg;
+      } else if (i + 1 < n) {
+        conv_box(i + 1, 1);
       }
       // this quarter's gamma_ij = e_ij 2^(m_h - M) / S; P = gamma 2^14
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
@@ -501,7 +520,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
 
       // ---- GEMM2(i-1) done: S' chunk complete (fold), Z and P free
       if (i >= 1) {
-        work_wait(&bars[B_G2_DONE], (i - 1) & 1, warp);
+        work_wait(&bars[B_G2_DONE], (i - 1) & 1);
         if (prev_fold) {
           fold(prev_b, chunk_start);
           tc_fence_before();
@@ -544,6 +563,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       if (lane == 0) mbar_arrive(&bars[B_P_FULL]);
       TRW(9);
       if (mt.flags & 1) {  // segment end: S0 (units of 2^14 gamma) -> s0 slot (cid + b)
+        float *s_s0 = s_s0_base + ((i + 1) & 1) * (4 * kTileM * 2);
         warp_transpose_reduce32(s0acc, lane);
         s_s0[q * kG + 32 * h + lane] = s0acc[0];
 #pragma unroll
@@ -558,7 +578,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       prev_fold = (mt.flags & 4) != 0;
     }
     if (n > 0) {  // last chunk
-      work_wait(&bars[B_G2_DONE], (n - 1) & 1, warp);
+      work_wait(&bars[B_G2_DONE], (n - 1) & 1);
       fold(prev_b, chunk_start);
     }
   }
