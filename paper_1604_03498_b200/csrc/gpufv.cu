@@ -81,9 +81,9 @@ int num_clusters(int C) {
 
 struct Layout {
   int C, Kp, ncl;
-  int64_t n_total, nslots;                                         // fold slots (append-only S' chunks)
+  int64_t n_total, nslots;                                         // segment slots (cluster, image)
   size_t wimg, bias, xshift, xscale, cshift, bscratch, coef;  // prepared GMM (head of ws)
-  size_t tiles, off1, norm2, s0slots, slots;              // per call
+  size_t tiles, off1, cstart, cown, norm2, s0slots, slots;  // per call
   size_t hx, hoff, hout;                                  // _host entry point
   size_t total;
 };
@@ -94,10 +94,9 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.Kp = L.C * kG;
   L.ncl = num_clusters(L.C);
   if (L.ncl <= 0) return false;
-  // total tiles <= n_total/128 + batch; fold chunk slots index tc/kFold + cid + b (k_stats.cuh)
-  const int64_t tmax = n_total / kTileM + batch + 1;
+  // one slot per (cluster, image) segment, index cid + b (seg_slot, fv_common.cuh)
   L.n_total = n_total;
-  L.nslots = tmax / kFold + 1 + L.ncl + batch;
+  L.nslots = (int64_t)L.ncl + batch + 1;
   size_t o = 0;
   L.wimg = o;     o = align_up(o + (size_t)L.C * kWImgBytes, 1024);
   L.bias = o;     o = align_up(o + (size_t)L.Kp * 4, 256);
@@ -108,6 +107,8 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.coef = o;     o = align_up(o + (size_t)3 * kDP * L.Kp * 8, 1024);
   L.tiles = o;    o = align_up(o + (size_t)(batch + 1) * 8, 256);
   L.off1 = o;     o = align_up(o + 16, 256);
+  L.cstart = o;   o = align_up(o + (size_t)(L.ncl + 1) * 4, 256);
+  L.cown = o;     o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 8, 256);
   L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 12, 1024);  // double norm2[] + uint counters[]
   L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * L.Kp * 4, 1024);
   L.slots = o;    o = align_up(o + (size_t)L.nslots * kNF * L.Kp * 4, 1024);
@@ -171,7 +172,8 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
                        int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st) {
   // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
   int64_t *off1 = (int64_t *)at(ws, L.off1);
-  k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles));
+  k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles), L.ncl,
+                                 (int *)at(ws, L.cstart), (int *)at(ws, L.cown));
   if (!offsets) offsets = off1;
   g_launches += 1;
   Stats2Params p;
@@ -251,6 +253,8 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.stats = nullptr;
   f.offsets = offsets;
   f.tile_start = (const int64_t *)at(ws, L.tiles);
+  f.cstart = (const int *)at(ws, L.cstart);
+  f.cown = (const int *)at(ws, L.cown);
   f.w = w;
   f.coef = (const double *)at(ws, L.coef);
   f.xscale = (const float *)at(ws, L.xscale);

@@ -114,9 +114,16 @@ __global__ void k_prep_w(const float *mu, const float *sg, int K, int D, int std
   *reinterpret_cast<__half *>(wimg + off + kOpBytes) = lo;
 }
 
+// Owner cluster of global tile t under the static split [c T / ncl, (c+1) T / ncl).
+__device__ __forceinline__ int64_t tile_owner(int64_t t, int64_t T, int64_t ncl) { return ((t + 1) * ncl - 1) / T; }
+
 // tile_start[0] = 0, tile_start[b+1] = sum_{b' <= b} ceil(N_b' / 128).  One block of 1024 threads.
 // offsets == nullptr means a single set of n_single rows: {0, n_single} is written to off1 and used.
-__global__ void k_schedule(const int64_t *offsets, int64_t *off1, int64_t n_single, int batch, int64_t *tile_start) {
+// Also the static split of the T tiles over the ncl clusters, for the finalize (no divisions there):
+//   cstart[c] = c T / ncl (c = 0..ncl);  cown[2b], cown[2b+1] = first / last cluster owning a tile of
+//   image b (last < first for an empty image).
+__global__ void k_schedule(const int64_t *offsets, int64_t *off1, int64_t n_single, int batch, int64_t *tile_start,
+                           int ncl, int *cstart, int *cown) {
   __shared__ int64_t s_warp[32];
   __shared__ int64_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -125,43 +132,54 @@ __global__ void k_schedule(const int64_t *offsets, int64_t *off1, int64_t n_sing
       off1[0] = 0; off1[1] = n_single;
       tile_start[0] = 0; tile_start[1] = (n_single + kTileM - 1) / kTileM;
     }
-    return;
+  } else {
+    if (tid == 0) { tile_start[0] = 0; s_carry = 0; }
+    __syncthreads();
+    for (int base = 0; base < batch; base += 1024) {
+      const int b = base + tid;
+      int64_t cnt = 0;
+      if (b < batch) {
+        int64_t n = offsets[b + 1] - offsets[b];
+        cnt = n > 0 ? (n + kTileM - 1) / kTileM : 0;
+      }
+      int64_t x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) { int64_t y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
+      if (lane == 31) s_warp[wid] = x;
+      __syncthreads();
+      if (wid == 0) {
+        int64_t y = s_warp[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { int64_t z = __shfl_up_sync(0xffffffffu, y, o); if (lane >= o) y += z; }
+        s_warp[lane] = y;
+      }
+      __syncthreads();
+      const int64_t incl = x + (wid > 0 ? s_warp[wid - 1] : 0) + s_carry;
+      if (b < batch) tile_start[b + 1] = incl;
+      __syncthreads();
+      if (tid == 1023) s_carry = incl;
+      __syncthreads();
+    }
   }
-  if (tid == 0) { tile_start[0] = 0; s_carry = 0; }
   __syncthreads();
-  for (int base = 0; base < batch; base += 1024) {
-    const int b = base + tid;
-    int64_t cnt = 0;
-    if (b < batch) {
-      int64_t n = offsets[b + 1] - offsets[b];
-      cnt = n > 0 ? (n + kTileM - 1) / kTileM : 0;
-    }
-    int64_t x = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) { int64_t y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
-    if (lane == 31) s_warp[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-      int64_t y = s_warp[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) { int64_t z = __shfl_up_sync(0xffffffffu, y, o); if (lane >= o) y += z; }
-      s_warp[lane] = y;
-    }
-    __syncthreads();
-    const int64_t incl = x + (wid > 0 ? s_warp[wid - 1] : 0) + s_carry;
-    if (b < batch) tile_start[b + 1] = incl;
-    __syncthreads();
-    if (tid == 1023) s_carry = incl;
-    __syncthreads();
+  const int64_t T = tile_start[batch];
+  for (int c = tid; c <= ncl; c += 1024) cstart[c] = (int)((int64_t)c * T / ncl);
+  for (int b = tid; b < batch; b += 1024) {
+    const int64_t ft = tile_start[b], lt = tile_start[b + 1];
+    int lo = 0, hi = -1;
+    if (ft < lt) { lo = (int)tile_owner(ft, T, ncl); hi = (int)tile_owner(lt - 1, T, ncl); }
+    cown[2 * b] = lo;
+    cown[2 * b + 1] = hi;
   }
 }
 
 struct FinParams {
-  const float *slots;         // fold slots from k_stats: nslots x kNF x Kp (nullptr when reading stats)
+  const float *slots;         // segment slots from k_stats: (ncl + batch) x kNF x Kp (nullptr: stats)
   const float *s0slots;       // (ncl + batch) x Kp
   const double *stats;        // batch x (1 + K(2D+1)) (nullptr when reading slots)
   const int64_t *offsets;     // batch + 1 (slots mode)
   const int64_t *tile_start;  // batch + 1 (slots mode)
+  const int *cstart, *cown;   // k_schedule: cluster tile split (ncl + 1), per-image owner range (2 batch)
   const float *w;
   const double *coef;         // 3 x kDP x Kp (k_prep_w)
   const float *xscale;
@@ -172,53 +190,34 @@ struct FinParams {
   int batch, K, Kp, D, ncl, mode;
 };
 
-// Owner cluster of global tile t under the static split [c T / ncl, (c+1) T / ncl).
-__device__ __forceinline__ int64_t tile_owner(int64_t t, int64_t T, int64_t ncl) { return ((t + 1) * ncl - 1) / T; }
-
 constexpr int kFinJ = 32;       // Gaussians per finalize block
 constexpr int kFinKI = kDP / 8; // dims per thread: k = kq + 8 i
-constexpr int kMaxSeg = 160;    // clusters one image can span (ncl <= SM count)
 
-// The (cluster, tile range) segments of image b, in ascending cluster order, computed once per block
-// by thread 0 (a6: the fixed-order reduction of the per-cluster pieces).
-struct SegTable {
-  int n;
-  int c[kMaxSeg], s0[kMaxSeg], s1[kMaxSeg];
-};
-__device__ __forceinline__ void seg_table(const FinParams &p, int b, SegTable &t) {
-  const int64_t T = p.tile_start[p.batch], ft = p.tile_start[b], lt = p.tile_start[b + 1];
-  int n = 0;
-  if (ft < lt) {
-    const int64_t clo = tile_owner(ft, T, p.ncl), chi = tile_owner(lt - 1, T, p.ncl);
-    for (int64_t c = clo; c <= chi && n < kMaxSeg; ++c) {
-      const int64_t st = c * T / p.ncl, en = (c + 1) * T / p.ncl;
-      const int64_t a = st > ft ? st : ft, e = en < lt ? en : lt;
-      if (a >= e) continue;
-      t.c[n] = (int)c; t.s0[n] = (int)a; t.s1[n] = (int)e; ++n;
-    }
-  }
-  t.n = n;
-}
-
-// S0_j (gamma units) and S1_jk, S2_jk (about c, unscaled; k = kq + 8 i) of image b from the slots.
-__device__ __forceinline__ void slot_sums(const FinParams &p, const SegTable &t, int b, int j, int kq, double &S0,
+// S0_j (gamma units) and S1_jk, S2_jk (about c, unscaled; k = kq + 8 i) of image b from the slots:
+// a6, the fixed-order reduction over the image's (cluster) segments in ascending cluster order.
+__device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int kq, double &S0,
                                           double (&S1)[kFinKI], double (&S2)[kFinKI]) {
   S0 = 0.0;
 #pragma unroll
   for (int i = 0; i < kFinKI; ++i) S1[i] = S2[i] = 0.0;
-  for (int g = 0; g < t.n; ++g) {
-    const int c = t.c[g];
-    S0 += (double)p.s0slots[(size_t)(c + b) * p.Kp + j];
-    for (int tc = t.s0[g]; tc < t.s1[g]; tc += kFold) {
-      const float *sl = p.slots + (size_t)fold_slot(tc, c, b) * kNF * p.Kp + j;
+  const int ft = (int)p.tile_start[b], lt = (int)p.tile_start[b + 1];
+  const int clo = p.cown[2 * b], chi = p.cown[2 * b + 1];
+  for (int c = clo; c <= chi; ++c) {
+    const int st = p.cstart[c], en = p.cstart[c + 1];
+    const int s0 = st > ft ? st : ft, s1 = en < lt ? en : lt;
+    if (s0 >= s1) continue;
+    S0 += (double)p.s0slots[(size_t)seg_slot(c, b) * p.Kp + j];
+    {
+      const float *sl = p.slots + (size_t)seg_slot(c, b) * kNF * p.Kp + j;
+      float v1[kFinKI], v2[kFinKI];
 #pragma unroll
       for (int i = 0; i < kFinKI; ++i) {
         const int k = kq + 8 * i;
-        if (k < p.D) {
-          S1[i] += (double)sl[(size_t)k * p.Kp];
-          S2[i] += (double)sl[(size_t)(kDP + k) * p.Kp];
-        }
+        v1[i] = k < p.D ? __ldcs(sl + (size_t)k * p.Kp) : 0.f;          // streamed: read once
+        v2[i] = k < p.D ? __ldcs(sl + (size_t)(kDP + k) * p.Kp) : 0.f;
       }
+#pragma unroll
+      for (int i = 0; i < kFinKI; ++i) { S1[i] += (double)v1[i]; S2[i] += (double)v2[i]; }
     }
   }
   S0 *= 1.0 / (double)kPScale;  // S0 was accumulated from P = gamma 2^14
@@ -238,22 +237,19 @@ __device__ __forceinline__ void slot_sums(const FinParams &p, const SegTable &t,
 // shared-memory tile so the global stores are coalesced over (j, k).  The Eq. (6)-(7) combination
 // runs in fp64; the signed square root (reading A9) in fp32 on the rounded value.  The L2 norm
 // is accumulated with one atomic per block and the LAST block of each image (ticket) rescales it.
-__global__ void __launch_bounds__(256) k_finalize(const FinParams p) {
+__global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
-  __shared__ SegTable s_seg;
   __shared__ double s_red[8];
   __shared__ int s_last;
   const int b = blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
   const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), j = j0 + jj;
   const int KD = p.K * p.D;
-  if (p.slots && tid == 0) seg_table(p, b, s_seg);
-  __syncthreads();
   double ss = 0.0;
   if (jj < nj) {
     double N, S0, S1[kFinKI], S2[kFinKI];
     if (p.slots) {
       N = (double)(p.offsets[b + 1] - p.offsets[b]);
-      slot_sums(p, s_seg, b, j, kq, S0, S1, S2);
+      slot_sums(p, b, j, kq, S0, S1, S2);
     } else {
       const double *st = p.stats + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
       N = st[0];
@@ -327,24 +323,27 @@ __global__ void __launch_bounds__(256) k_finalize(const FinParams p) {
   if (!(n2 > 0.0)) return;
   const float sc = (float)(1.0 / sqrt(n2));
   float4 *ob = reinterpret_cast<float4 *>(p.out + (size_t)b * 2 * KD);  // 2KD % 4 == 0 (D % 4 == 0)
-  for (int t = tid; t < (2 * KD) / 4; t += 256) {
-    float4 v = __ldcg(ob + t);
-    v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
-    ob[t] = v;
+  const int n4 = (2 * KD) / 4;
+  for (int t0 = 0; t0 < n4; t0 += 256 * 8) {  // 8 loads in flight per thread (the image is in L2)
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { const int t = t0 + u * 256 + tid; if (t < n4) v[u] = __ldcg(ob + t); }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * 256 + tid;
+      if (t < n4) { v[u].x *= sc; v[u].y *= sc; v[u].z *= sc; v[u].w *= sc; ob[t] = v[u]; }
+    }
   }
 }
 
 // a6 only: slots -> fp64 stats [N, S0, S1, S2] about c (reading A19).  Same grid as k_finalize.
 __global__ void __launch_bounds__(256) k_reduce_stats(const FinParams p) {
-  __shared__ SegTable s_seg;
   const int b = blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
   const int j = blockIdx.x * kFinJ + jj;
-  if (tid == 0) seg_table(p, b, s_seg);
-  __syncthreads();
   if (j >= p.K) return;
   const int KD = p.K * p.D;
   double S0, S1[kFinKI], S2[kFinKI];
-  slot_sums(p, s_seg, b, j, kq, S0, S1, S2);
+  slot_sums(p, b, j, kq, S0, S1, S2);
   double *st = p.stats_out + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
   if (blockIdx.x == 0 && tid == 0) st[0] = (double)(p.offsets[b + 1] - p.offsets[b]);
   if (kq == 0) st[1 + j] = S0;

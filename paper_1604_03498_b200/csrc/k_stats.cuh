@@ -44,7 +44,7 @@ constexpr int kMaxC2 = 4;                        // K <= 512 in this kernel
 
 // per-tile metadata published by the TMA thread (ring of 4: slot t % 4 stays valid well past tile t)
 struct TileMeta {
-  int row0, nrows, b, t, flags;  // flags: 1 seg_last, 2 chunk_first, 4 fold
+  int row0, nrows, b, t, flags;  // flags: 1 seg_last, 2 chunk_first, 4 fold, 8 seg_first
 };
 
 // shared memory map (offsets from a 1024-aligned base)
@@ -85,7 +85,7 @@ struct Stats2Params {
   const uint8_t *wimg;        // C x kWImgBytes
   const float *bias;          // Kp
   const float *xshift, *xscale;
-  float *slots;               // fold slots: nslots x kNF x Kp   (feature-major rows)
+  float *slots;               // segment slots: (ncl + batch) x kNF x Kp   (feature-major rows)
   float *s0slots;             // (ncl + batch) x Kp
   float *gamma_out;
   long long *trace;           // debug (GPUFV_TRACE builds): per-tile phase clocks of CTA 0
@@ -123,7 +123,7 @@ struct TileWalker {
     const int rem = off_b1 - m.row0;
     m.nrows = rem < kTileM ? rem : kTileM;
     const bool seg_last = (t + 1 == t1) || (t + 1 >= ts_b1);
-    m.flags = (seg_last ? 1 : 0) | ((seg_pos % kFold) == 0 ? 2 : 0) |
+    m.flags = (seg_last ? 1 : 0) | ((seg_pos % kFold) == 0 ? 2 : 0) | (seg_pos == 0 ? 8 : 0) |
               ((seg_last || (seg_pos + 1) % kFold == 0) ? 4 : 0);
     return m;
   }
@@ -396,23 +396,32 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         sts128(sZ + kOpBytes + kAtomBytes + o, zb[12], zb[13], zb[14], zb[15]);
       }
     };
-    auto fold = [&](int b, int chunk_start) {  // S' quarter (lane = feature, columns 32h..) -> slot
-      float *dst = p.slots + (size_t)fold_slot(chunk_start, cid, b) * kNF * p.Kp + (size_t)row * p.Kp + rank * kG + 32 * h;
+    // S' quarter (lane = feature, columns 32h..) of a finished chunk -> the segment slot: stored by
+    // the segment's first chunk, added (red.global.add.v4.f32, same thread, program order) by the rest
+    auto fold = [&](int b, bool first) {
+      float *dst = p.slots + (size_t)seg_slot(cid, b) * kNF * p.Kp + (size_t)row * p.Kp + rank * kG + 32 * h;
       uint32_t v[32];
       tmem_ld32(tmem + kTS + lane_base + 32 * h, v);
       tmem_ld_wait(v);
-      float4 *d4 = reinterpret_cast<float4 *>(dst);
+      if (first) {
+        float4 *d4 = reinterpret_cast<float4 *>(dst);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
-                            __uint_as_float(v[4 * j + 3]));
+        for (int j = 0; j < 8; ++j)
+          d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
+                              __uint_as_float(v[4 * j + 3]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          red_add_v4(dst + 4 * j, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                     __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+      }
     };
 
     float s0acc[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) s0acc[j] = 0.f;
-    int chunk_start = t0, prev_b = 0;
-    bool prev_fold = false;
+    int prev_b = 0;
+    bool prev_fold = false, chunk_seg_first = true;
     if (n > 0) { conv_box(0, 0); conv_box(0, 1); }
     for (int i = 0; i < n; ++i) {
       TRW(0);
@@ -522,14 +531,14 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       if (i >= 1) {
         work_wait(&bars[B_G2_DONE], (i - 1) & 1);
         if (prev_fold) {
-          fold(prev_b, chunk_start);
+          fold(prev_b, chunk_seg_first);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars[B_FOLD_DONE]);
         }
       }
       TRW(7);
-      if (mt.flags & 2) chunk_start = mt.t;
+      if (mt.flags & 2) chunk_seg_first = (mt.flags & 8) != 0;
 
       // ---- P(i) = gamma 2^14 (thresholded: gamma <= tau -> 0) -> fp16 hi/lo, S0 accumulation
       const float2 ap = make_float2(alpha_p, alpha_p);
@@ -570,7 +579,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         for (int j = 0; j < 32; ++j) s0acc[j] = 0.f;
         named_bar_sync(kBarWork, kWarpsWork * 32);
         if (tid < kG)
-          p.s0slots[(size_t)(cid + mt.b) * p.Kp + rank * kG + tid] =
+          p.s0slots[(size_t)seg_slot(cid, mt.b) * p.Kp + rank * kG + tid] =
               (s_s0[tid] + s_s0[kG + tid]) + (s_s0[2 * kG + tid] + s_s0[3 * kG + tid]);
         named_bar_sync(kBarWork, kWarpsWork * 32);
       }
@@ -579,7 +588,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     }
     if (n > 0) {  // last chunk
       work_wait(&bars[B_G2_DONE], (n - 1) & 1);
-      fold(prev_b, chunk_start);
+      fold(prev_b, chunk_seg_first);
     }
   }
 
