@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdarg>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -262,6 +263,7 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.stats_out = nullptr;
   f.norm2 = (double *)at(ws, L.norm2);
   f.counters = (unsigned *)(f.norm2 + (batch > 0 ? batch : 1));
+  f.b_base = 0;
   f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
   f.mode = (int)(flags & FV_NORM_MASK);
   return f;
@@ -271,8 +273,12 @@ fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStrea
   (void)D;
   if (batch == 0) return FV_OK;
   if (cudaMemsetAsync(f.norm2, 0, (size_t)batch * 12, st) != cudaSuccess) return cuda_check("memset norm2");
-  k_finalize<<<dim3((K + kFinJ - 1) / kFinJ, batch), 256, 0, st>>>(f);
-  g_launches += 1;
+  for (int b0 = 0; b0 < batch; b0 += 65535) {  // gridDim.y limit
+    FinParams fc = f;
+    fc.b_base = b0;
+    k_finalize<<<dim3((K + kFinJ - 1) / kFinJ, std::min(65535, batch - b0)), 256, 0, st>>>(fc);
+    g_launches += 1;
+  }
   return cuda_check("k_finalize");
 }
 
@@ -401,8 +407,12 @@ fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, in
   if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st)) return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   f.stats_out = stats;
-  k_reduce_stats<<<dim3((K + kFinJ - 1) / kFinJ, batch), 256, 0, st>>>(f);
-  g_launches += 1;
+  for (int b0 = 0; b0 < batch; b0 += 65535) {
+    FinParams fc = f;
+    fc.b_base = b0;
+    k_reduce_stats<<<dim3((K + kFinJ - 1) / kFinJ, std::min(65535, batch - b0)), 256, 0, st>>>(fc);
+    g_launches += 1;
+  }
   return cuda_check("k_reduce_stats");
 }
 

@@ -188,6 +188,7 @@ struct FinParams {
   double *norm2;              // batch (zeroed before k_finalize)
   unsigned *counters;         // batch (zeroed before k_finalize): last-block ticket
   int batch, K, Kp, D, ncl, mode;
+  int b_base;                 // first image of this launch (gridDim.y <= 65535 images per launch)
 };
 
 constexpr int kFinJ = 32;       // Gaussians per finalize block
@@ -232,58 +233,113 @@ __device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int 
   }
 }
 
-// grid (ceil(K/32), batch), 256 threads.  Thread (jj = tid % 32, kq = tid / 32) owns Gaussian
-// j0 + jj and dims kq + 8 i: slot and coefficient reads are coalesced over jj; U/V go through a
-// shared-memory tile so the global stores are coalesced over (j, k).  The Eq. (6)-(7) combination
-// runs in fp64; the signed square root (reading A9) in fp32 on the rounded value.  The L2 norm
-// is accumulated with one atomic per block and the LAST block of each image (ticket) rescales it.
+// grid (ceil(K/32), batch), 256 threads.  Thread (jq = tid % 8, kr = tid / 8) owns Gaussians
+// j0 + 4 jq .. +3 and dims kr, kr + 32: every slot / coefficient read is a 16-byte vector, coalesced
+// over jq (the slots are feature-major rows of Kp Gaussians); U/V go through a shared-memory tile so
+// the global stores are coalesced over (j, k).  The Eq. (6)-(7) combination runs in fp64; the signed
+// square root (reading A9) in fp32 on the rounded value.  The L2 norm is accumulated with one
+// atomic per block and the LAST block of each image (ticket) rescales it.
+constexpr int kFinKR = 2;  // dims per thread (kr, kr + 32)
 __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
   __shared__ double s_red[8];
   __shared__ int s_last;
-  const int b = blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
-  const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), j = j0 + jj;
+  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, jq = tid & 7, kr = tid >> 3;
+  const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
   const int KD = p.K * p.D;
   double ss = 0.0;
-  if (jj < nj) {
-    double N, S0, S1[kFinKI], S2[kFinKI];
+  if (4 * jq < nj) {
+    double N, S0[4], S1[kFinKR][4], S2[kFinKR][4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      S0[e] = 0.0;
+#pragma unroll
+      for (int r = 0; r < kFinKR; ++r) S1[r][e] = S2[r][e] = 0.0;
+    }
     if (p.slots) {
+      // a6: the image's (cluster) segments in ascending cluster order
       N = (double)(p.offsets[b + 1] - p.offsets[b]);
-      slot_sums(p, b, j, kq, S0, S1, S2);
+      const int ft = (int)p.tile_start[b], lt = (int)p.tile_start[b + 1];
+      const int clo = p.cown[2 * b], chi = p.cown[2 * b + 1];
+      for (int c = clo; c <= chi; ++c) {
+        const int st = p.cstart[c], en = p.cstart[c + 1];
+        if ((st > ft ? st : ft) >= (en < lt ? en : lt)) continue;
+        const size_t seg = (size_t)seg_slot(c, b);
+        const float4 s0 = __ldcs(reinterpret_cast<const float4 *>(p.s0slots + seg * p.Kp + jb));
+        const float *sl = p.slots + seg * kNF * p.Kp + jb;
+        float4 v1[kFinKR], v2[kFinKR];
+#pragma unroll
+        for (int r = 0; r < kFinKR; ++r) {
+          const int k = kr + 32 * r;
+          v1[r] = __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)k * p.Kp));           // streamed once
+          v2[r] = __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)(kDP + k) * p.Kp));
+        }
+        S0[0] += (double)s0.x; S0[1] += (double)s0.y; S0[2] += (double)s0.z; S0[3] += (double)s0.w;
+#pragma unroll
+        for (int r = 0; r < kFinKR; ++r) {
+          S1[r][0] += (double)v1[r].x; S1[r][1] += (double)v1[r].y; S1[r][2] += (double)v1[r].z; S1[r][3] += (double)v1[r].w;
+          S2[r][0] += (double)v2[r].x; S2[r][1] += (double)v2[r].y; S2[r][2] += (double)v2[r].z; S2[r][3] += (double)v2[r].w;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) S0[e] *= 1.0 / (double)kPScale;  // S0 was accumulated from P = gamma 2^14
+#pragma unroll
+      for (int r = 0; r < kFinKR; ++r) {
+        const int k = kr + 32 * r;
+        const double xs = 1.0 / ((double)kPScale * (double)p.xscale[k]);  // powers of two: exact
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { S1[r][e] *= xs; S2[r][e] *= xs * xs * (double)kPScale; }
+      }
     } else {
       const double *st = p.stats + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
       N = st[0];
-      S0 = st[1 + j];
 #pragma unroll
-      for (int i = 0; i < kFinKI; ++i) {
-        const int k = kq + 8 * i;
-        S1[i] = S2[i] = 0.0;
-        if (k < p.D) {
-          S1[i] = st[1 + p.K + (size_t)j * p.D + k];
-          S2[i] = st[1 + p.K + (size_t)KD + (size_t)j * p.D + k];
+      for (int e = 0; e < 4; ++e) {
+        const int j = jb + e;
+        if (j >= p.K) continue;
+        S0[e] = st[1 + j];
+#pragma unroll
+        for (int r = 0; r < kFinKR; ++r) {
+          const int k = kr + 32 * r;
+          if (k < p.D) {
+            S1[r][e] = st[1 + p.K + (size_t)j * p.D + k];
+            S2[r][e] = st[1 + p.K + (size_t)KD + (size_t)j * p.D + k];
+          }
         }
       }
     }
-    double fu = 1.0, fv = 1.0;
-    if (p.mode == 0 && N > 0.0) {
-      const double pj = (double)p.w[j];
-      fu = 1.0 / (N * sqrt(pj));
-      fv = 1.0 / (N * sqrt(2.0 * pj));
+    double fu[4], fv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      fu[e] = fv[e] = 1.0;
+      if (p.mode == 0 && N > 0.0 && jb + e < p.K) {
+        const double pj = (double)p.w[jb + e];
+        fu[e] = 1.0 / (N * sqrt(pj));
+        fv[e] = 1.0 / (N * sqrt(2.0 * pj));
+      }
     }
     const bool zero = (p.mode != 2) && !(N > 0.0);
 #pragma unroll
-    for (int i = 0; i < kFinKI; ++i) {
-      const int k = kq + 8 * i;
-      if (k < p.D) {
-        const double mup = p.coef[(size_t)k * p.Kp + j];
-        const double isd = p.coef[(size_t)(kDP + k) * p.Kp + j];
-        const double ivar = p.coef[(size_t)(2 * kDP + k) * p.Kp + j];
-        double U = (S1[i] - mup * S0) * isd;                                 // sum gamma (x - mu)/sd
-        double V = (S2[i] - 2.0 * mup * S1[i] + mup * mup * S0) * ivar - S0;  // sum gamma ((x-mu)^2/var - 1)
+    for (int r = 0; r < kFinKR; ++r) {
+      const int k = kr + 32 * r;
+      if (k >= p.D) continue;
+      const double *cf = p.coef + (size_t)k * p.Kp + jb;
+      const double2 m01 = *reinterpret_cast<const double2 *>(cf), m23 = *reinterpret_cast<const double2 *>(cf + 2);
+      const double2 i01 = *reinterpret_cast<const double2 *>(cf + kDP * p.Kp);
+      const double2 i23 = *reinterpret_cast<const double2 *>(cf + kDP * p.Kp + 2);
+      const double2 v01 = *reinterpret_cast<const double2 *>(cf + 2 * kDP * p.Kp);
+      const double2 v23 = *reinterpret_cast<const double2 *>(cf + 2 * kDP * p.Kp + 2);
+      const double mup[4] = {m01.x, m01.y, m23.x, m23.y}, isd[4] = {i01.x, i01.y, i23.x, i23.y},
+                   ivar[4] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (4 * jq + e >= nj) continue;
+        double U = (S1[r][e] - mup[e] * S0[e]) * isd[e];                                       // sum gamma (x - mu)/sd
+        double V = (S2[r][e] - 2.0 * mup[e] * S1[r][e] + mup[e] * mup[e] * S0[e]) * ivar[e] - S0[e];  // ((x-mu)^2/var - 1)
         float u, v;
         if (p.mode != 2) {
-          U = zero ? 0.0 : U * fu;
-          V = zero ? 0.0 : V * fv;
+          U = zero ? 0.0 : U * fu[e];
+          V = zero ? 0.0 : V * fv[e];
           ss += fabs(U) + fabs(V);  // = (signed sqrt)^2
           u = copysignf(sqrtf(fabsf((float)U)), (float)U);
           v = copysignf(sqrtf(fabsf((float)V)), (float)V);
@@ -291,8 +347,8 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
           u = (float)U;
           v = (float)V;
         }
-        sU[jj][k] = u;
-        sV[jj][k] = v;
+        sU[4 * jq + e][k] = u;
+        sV[4 * jq + e][k] = v;
       }
     }
   }
@@ -338,7 +394,7 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
 
 // a6 only: slots -> fp64 stats [N, S0, S1, S2] about c (reading A19).  Same grid as k_finalize.
 __global__ void __launch_bounds__(256) k_reduce_stats(const FinParams p) {
-  const int b = blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
+  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
   const int j = blockIdx.x * kFinJ + jj;
   if (j >= p.K) return;
   const int KD = p.K * p.D;
