@@ -17,9 +17,12 @@
  *   - Array arguments are CUDA DEVICE pointers on the current device unless the name ends in _host.
  *     The library never allocates, frees or synchronises on the device paths; all work is enqueued
  *     asynchronously on `stream` (NULL = legacy default stream).  The caller owns every buffer.
- *   - fp32 in, fp32 out; internal statistics are reduced in fp64.  Results are deterministic
- *     (static schedule + fixed-order reductions): identical inputs give bitwise-identical outputs.
- *   - Limits: 1 <= K <= 512, 1 <= D <= 64, D % 4 == 0 (caller pads, reading A13), X 16-byte aligned.
+ *   - fp32 in, fp32 out.  Sufficient statistics accumulate on the tensor cores in fp32 chunks of <= 16
+ *     tiles that are added, in a fixed program order, into one fp32 slot per (cluster, image); slots are
+ *     combined and normalised in fp64.  Results are deterministic (static schedule + fixed-order
+ *     reductions): identical inputs give bitwise-identical outputs.
+ *   - Limits: 1 <= K <= 512, 1 <= D <= 128, D % 4 == 0 (caller pads, reading A13), X 16-byte aligned.
+ *     D <= 64 runs the narrow kernel (128 Gaussians per CTA); 64 < D <= 128 the wide one (64 per CTA).
  *   - Device data is not validated (that would need a kernel + sync): var <= 0, pi <= 0 or non-finite
  *     X propagate NaN into that image's output only.  Descriptors with |x-c|/rms >= 255 in some
  *     dimension (c, rms: GMM-weighted mean/RMS) overflow the fp16 split operands.
@@ -42,7 +45,7 @@ typedef struct CUstream_st *fv_stream_t; /* == cudaStream_t */
 typedef enum {
   FV_OK = 0,
   FV_ERR_ARG = 1,         /* null pointer, N/batch < 0, K < 1, D < 1, threshold NaN or >= 1, bad flags */
-  FV_ERR_UNSUPPORTED = 2, /* K > 512, D > 64, D % 4 != 0, misaligned X, device is not sm_100      */
+  FV_ERR_UNSUPPORTED = 2, /* K > 512, D > 128, D % 4 != 0, misaligned X, device is not sm_100     */
   FV_ERR_WORKSPACE = 3,   /* ws_bytes < fv_workspace_bytes(...) or ws misaligned (needs 1024 B)    */
   FV_ERR_CUDA = 4         /* a CUDA launch/runtime call failed (detail in fv_last_error())          */
 } fv_status;

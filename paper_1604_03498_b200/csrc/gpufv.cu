@@ -17,6 +17,7 @@
 #include "fv_common.cuh"
 #include "k_aux.cuh"
 #include "k_stats.cuh"
+#include "k_stats_w.cuh"
 
 using namespace gpufv;
 
@@ -45,18 +46,25 @@ fv_status cuda_check(const char *what) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-int cluster_size(int K) { return (K + kG - 1) / kG; }
+// Tile family: D <= 64 -> k_stats (128 Gaussians per CTA, cluster <= 4); 64 < D <= 128 -> k_stats_w
+// (64 Gaussians per CTA, cluster <= 8).  K <= 512 for both.
+bool is_wide(int D) { return D > kDP; }
+int gauss_per_cta(int D) { return is_wide(D) ? kGW : kG; }
+int cluster_size(int K, int D) { return (K + gauss_per_cta(D) - 1) / gauss_per_cta(D); }
 
-// Persistent grid: the number of co-resident clusters of k_stats on the current device.
-int num_clusters(int C) {
+// Persistent grid: the number of co-resident clusters of the stats kernel on the current device.
+int num_clusters(int C, bool wide) {
   static std::mutex mu;
-  static int cache[64][kMaxC2 + 1] = {};
+  static int cache[64][2][kMaxCW + 1] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
   std::lock_guard<std::mutex> lk(mu);
-  if (cache[dev][C] > 0) return cache[dev][C];
+  if (cache[dev][wide][C] > 0) return cache[dev][wide][C];
+  const int smem = wide ? kSmemWBytes : kSmem2Bytes;
   if (cudaFuncSetAttribute(k_stats<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess)
+      cudaFuncSetAttribute(k_stats<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess)
     return -1;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -66,22 +74,24 @@ int num_clusters(int C) {
   attr[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3(C * 148, 1, 1);
   cfg.blockDim = dim3(kThreads2, 1, 1);
-  cfg.dynamicSmemBytes = kSmem2Bytes;
+  cfg.dynamicSmemBytes = smem;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_stats<true>, &cfg) != cudaSuccess || n <= 0) {
+  const cudaError_t e = wide ? cudaOccupancyMaxActiveClusters(&n, k_stats_w<true>, &cfg)
+                             : cudaOccupancyMaxActiveClusters(&n, k_stats<true>, &cfg);
+  if (e != cudaSuccess || n <= 0) {
     cudaGetLastError();
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     n = sms / C;
   }
-  cache[dev][C] = n;
+  cache[dev][wide][C] = n;
   return n;
 }
 
 struct Layout {
-  int C, Kp, ncl;
+  int C, Kp, ncl, dpad;  // cluster size, padded K, clusters, padded D (64 | 128)
   int64_t n_total, nslots;                                         // segment slots (cluster, image)
   size_t wimg, bias, xshift, xscale, cshift, bscratch, coef;  // prepared GMM (head of ws)
   size_t tiles, off1, cstart, cown, norm2, s0slots, slots;  // per call
@@ -90,10 +100,10 @@ struct Layout {
 };
 
 bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout &L) {
-  (void)D;
-  L.C = cluster_size(K);
-  L.Kp = L.C * kG;
-  L.ncl = num_clusters(L.C);
+  L.C = cluster_size(K, D);
+  L.Kp = L.C * gauss_per_cta(D);
+  L.dpad = is_wide(D) ? kDMax : kDP;
+  L.ncl = num_clusters(L.C, is_wide(D));
   if (L.ncl <= 0) return false;
   // one slot per (cluster, image) segment, index cid + b (seg_slot, fv_common.cuh)
   L.n_total = n_total;
@@ -101,18 +111,18 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   size_t o = 0;
   L.wimg = o;     o = align_up(o + (size_t)L.C * kWImgBytes, 1024);
   L.bias = o;     o = align_up(o + (size_t)L.Kp * 4, 256);
-  L.xshift = o;   o = align_up(o + kDP * 4, 256);
-  L.xscale = o;   o = align_up(o + kDP * 4, 256);
-  L.cshift = o;   o = align_up(o + kDP * 8, 256);
+  L.xshift = o;   o = align_up(o + kDMax * 4, 256);
+  L.xscale = o;   o = align_up(o + kDMax * 4, 256);
+  L.cshift = o;   o = align_up(o + kDMax * 8, 256);
   L.bscratch = o; o = align_up(o + (size_t)L.Kp * 8, 1024);
-  L.coef = o;     o = align_up(o + (size_t)3 * kDP * L.Kp * 8, 1024);
+  L.coef = o;     o = align_up(o + (size_t)3 * kDMax * L.Kp * 8, 1024);
   L.tiles = o;    o = align_up(o + (size_t)(batch + 1) * 8, 256);
   L.off1 = o;     o = align_up(o + 16, 256);
   L.cstart = o;   o = align_up(o + (size_t)(L.ncl + 1) * 4, 256);
   L.cown = o;     o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 8, 256);
   L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 12, 1024);  // double norm2[] + uint counters[]
   L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * L.Kp * 4, 1024);
-  L.slots = o;    o = align_up(o + (size_t)L.nslots * kNF * L.Kp * 4, 1024);
+  L.slots = o;    o = align_up(o + (size_t)L.nslots * 2 * L.dpad * L.Kp * 4, 1024);
   L.hx = L.hoff = L.hout = 0;
   if (host_io) {
     L.hx = o;   o = align_up(o + (size_t)n_total * D * 4, 1024);
@@ -126,8 +136,8 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
 fv_status check_gmm_args(int K, int D, const float *w, const float *mu, const float *sg, unsigned flags) {
   if (!w || !mu || !sg) return fail(FV_ERR_ARG, "null GMM pointer");
   if (K < 1 || D < 1) return fail(FV_ERR_ARG, "K=%d and D=%d must be >= 1", K, D);
-  if (K > kG * kMaxC2) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kG * kMaxC2);
-  if (D > kDP) return fail(FV_ERR_UNSUPPORTED, "D=%d > %d", D, kDP);
+  if (K > kG * kMaxC2) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kG * kMaxC2);  // 512 for both tile families
+  if (D > kDMax) return fail(FV_ERR_UNSUPPORTED, "D=%d > %d", D, kDMax);
   if (D % 4 != 0) return fail(FV_ERR_UNSUPPORTED, "D=%d is not a multiple of 4 (pad, reading A13)", D);
   const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED;
   if (flags & ~known) return fail(FV_ERR_ARG, "unknown flag bits 0x%x", flags & ~known);
@@ -162,8 +172,8 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
   const int sd = (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0;
   k_prep_shift<<<1, 256, 0, st>>>(w, mu, sg, K, D, L.Kp, sd, (double *)at(ws, L.cshift), (float *)at(ws, L.xshift),
                                   (float *)at(ws, L.xscale), (float *)at(ws, L.bias), (double *)at(ws, L.bscratch));
-  k_prep_w<<<L.Kp, kNF, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
-                                 at(ws, L.wimg), (double *)at(ws, L.coef));
+  k_prep_w<<<L.Kp, 2 * L.dpad, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
+                                 at(ws, L.wimg), (double *)at(ws, L.coef), is_wide(D) ? 1 : 0);
   g_launches += 2;
   return cuda_check("k_prep");
 }
@@ -224,12 +234,14 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   attr[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3(L.C * L.ncl, 1, 1);
   cfg.blockDim = dim3(kThreads2, 1, 1);
-  cfg.dynamicSmemBytes = kSmem2Bytes;
+  cfg.dynamicSmemBytes = is_wide(D) ? kSmemWBytes : kSmem2Bytes;
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (g_prof_start) cudaEventRecord(g_prof_start, st);
-  cudaError_t e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false>, tmap, p);
+  cudaError_t e;
+  if (!is_wide(D)) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false>, tmap, p);
+  else e = (D == kDMax) ? cudaLaunchKernelEx(&cfg, k_stats_w<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false>, tmap, p);
   if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
   g_launches += 1;
   if (e != cudaSuccess) {
@@ -239,7 +251,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
     return fail(FV_ERR_CUDA,
                 "k_stats launch: %s (grid %d x %d threads, cluster %d, dyn smem %d; kernel: %d regs, max threads %d, "
                 "local %zu B, static smem %zu B, max dyn smem %d)",
-                cudaGetErrorString(e), L.C * L.ncl, kThreads2, L.C, kSmem2Bytes, fa.numRegs, fa.maxThreadsPerBlock,
+                cudaGetErrorString(e), L.C * L.ncl, kThreads2, L.C, (int)cfg.dynamicSmemBytes, fa.numRegs, fa.maxThreadsPerBlock,
                 fa.localSizeBytes, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes);
   }
   return cuda_check("k_stats");
@@ -266,17 +278,18 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.b_base = 0;
   f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
   f.mode = (int)(flags & FV_NORM_MASK);
+  f.dpad = L.dpad;
   return f;
 }
 
 fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStream_t st) {
-  (void)D;
+
   if (batch == 0) return FV_OK;
   if (cudaMemsetAsync(f.norm2, 0, (size_t)batch * 12, st) != cudaSuccess) return cuda_check("memset norm2");
   for (int b0 = 0; b0 < batch; b0 += 65535) {  // gridDim.y limit
     FinParams fc = f;
     fc.b_base = b0;
-    k_finalize<<<dim3((K + kFinJ - 1) / kFinJ, std::min(65535, batch - b0)), 256, 0, st>>>(fc);
+    k_finalize<<<dim3((K + kFinJ - 1) / kFinJ, std::min(65535, batch - b0), (D + kDP - 1) / kDP), 256, 0, st>>>(fc);
     g_launches += 1;
   }
   return cuda_check("k_finalize");
@@ -410,7 +423,7 @@ fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, in
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     FinParams fc = f;
     fc.b_base = b0;
-    k_reduce_stats<<<dim3((K + kFinJ - 1) / kFinJ, std::min(65535, batch - b0)), 256, 0, st>>>(fc);
+    k_reduce_stats<<<dim3((K + kFinJ - 1) / kFinJ, std::min(65535, batch - b0), (D + kDP - 1) / kDP), 256, 0, st>>>(fc);
     g_launches += 1;
   }
   return cuda_check("k_reduce_stats");

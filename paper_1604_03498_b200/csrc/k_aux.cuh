@@ -26,10 +26,10 @@ __device__ __forceinline__ double gmm_var(const float *sigmas, size_t i, bool st
 __global__ void k_prep_shift(const float *w, const float *mu, const float *sg, int K, int D, int Kp,
                              int stddev, double *cshift, float *xshift, float *xscale, float *bias,
                              double *bscratch) {
-  __shared__ double s_c[kDP];
+  __shared__ double s_c[kDMax];
   __shared__ double s_red[256];
   const int tid = threadIdx.x;
-  if (tid < kDP) {
+  if (tid < kDMax) {
     double c = 0.0, sc = 1.0;
     if (tid < D) {
       double ws = 0.0, acc = 0.0;
@@ -77,41 +77,55 @@ __global__ void k_prep_shift(const float *w, const float *mu, const float *sg, i
 
 // a1 (part 2): W'_jf (log2 units, scaled by the feature exponents) split into fp16 hi/lo and stored
 // as the exact SWIZZLE_128B K-major shared-memory image each CTA rank bulk-copies:
-//   f <  64:  W'_jk      =  log2e (mu_jk - c_k) / var_jk * 2^-e_k
-//   f >= 64:  W'_j,64+k  = -log2e / (2 var_jk)          * 2^-2e_k
-// grid = Kp blocks (one Gaussian each), 128 threads (one feature each).
-//
-// Also writes the finalize coefficients coef[3][kDP][Kp] (a7, Eq. (6)-(7) of P:141-152 expanded about c):
+//   lin  feature of dim k:  W' =  log2e (mu_jk - c_k) / var_jk * 2^-e_k
+//   quad feature of dim k:  W' = -log2e / (2 var_jk)          * 2^-2e_k
+// Narrow (D <= 64, k_stats): 128 Gaussians per rank, features f = [lin 0..63 | quad 0..63], image =
+//   [hi | lo] x 2 atoms (64 features) x 128 rows x 128 B.
+// Wide (D <= 128, k_stats_w): 64 Gaussians per rank, two feature halves hf = 0, 1 of the dims
+//   [64 hf, 64 hf + 64), each [lin | quad]; image = 2 halves x [hi | lo] x 2 atoms x 64 rows x 128 B.
+// grid = Kp blocks (one Gaussian each), 2 dpad threads (one feature each).
+// Also writes the finalize coefficients coef[3][kDMax][Kp] (a7, Eq. (6)-(7) of P:141-152 expanded about c):
 //   coef[0][k][j] = mu_jk - c_k,  coef[1][k][j] = 1 / sqrt(var_jk),  coef[2][k][j] = 1 / var_jk
 // (Gaussian-fastest so the finalize reads them coalesced; zero for padded j / k).
 __global__ void k_prep_w(const float *mu, const float *sg, int K, int D, int stddev, const double *cshift,
-                         const float *xscale, uint8_t *wimg, double *coef) {
+                         const float *xscale, uint8_t *wimg, double *coef, int wide) {
   const int j = blockIdx.x, f = threadIdx.x, Kp = gridDim.x;
-  const int k = f & (kDP - 1);
+  int k, lin, off;
+  if (!wide) {
+    lin = f < kDP;
+    k = f & (kDP - 1);
+    const int rank = j / kG, row = j % kG, atom = f / 64, chunk = (f & 63) >> 3, e = f & 7;
+    off = rank * kWImgBytes + atom * kAtomBytes + row * 128 + ((chunk ^ (row & 7)) << 4) + e * 2;
+  } else {
+    const int hf = f / kNF, fh = f % kNF;
+    lin = fh < kDP;
+    k = kDP * hf + (fh & (kDP - 1));
+    const int rank = j / kGW, row = j % kGW, atom = fh / 64, chunk = (fh & 63) >> 3, e = fh & 7;
+    off = rank * kWImgBytes + hf * (kWImgBytes / 2) + atom * (kGW * 128) + row * 128 + ((chunk ^ (row & 7)) << 4) + e * 2;
+  }
+  const int lo_off = wide ? kGW * 128 * 2 : kOpBytes;  // lo half after the 2 hi atoms
   double wv = 0.0;
   if (j < K && k < D) {
     const double v = gmm_var(sg, (size_t)j * D + k, stddev);
     const double s = (double)xscale[k];
     const double mup = (double)mu[(size_t)j * D + k] - cshift[k];
-    if (f < kDP) wv = kLog2e * mup / v / s;
+    if (lin) wv = kLog2e * mup / v / s;
     else wv = -kLog2e / (2.0 * v) / (s * s);
-    if (f < kDP) {
+    if (lin) {
       coef[(size_t)k * Kp + j] = mup;
-      coef[(size_t)(kDP + k) * Kp + j] = 1.0 / sqrt(v);
-      coef[(size_t)(2 * kDP + k) * Kp + j] = 1.0 / v;
+      coef[(size_t)(kDMax + k) * Kp + j] = 1.0 / sqrt(v);
+      coef[(size_t)(2 * kDMax + k) * Kp + j] = 1.0 / v;
     }
-  } else if (f < kDP) {
+  } else if (lin) {
     coef[(size_t)k * Kp + j] = 0.0;
-    coef[(size_t)(kDP + k) * Kp + j] = 0.0;
-    coef[(size_t)(2 * kDP + k) * Kp + j] = 0.0;
+    coef[(size_t)(kDMax + k) * Kp + j] = 0.0;
+    coef[(size_t)(2 * kDMax + k) * Kp + j] = 0.0;
   }
   const float w32 = (float)wv;
   const __half hi = __float2half_rn(w32);
   const __half lo = __float2half_rn(w32 - __half2float(hi));
-  const int rank = j / kG, row = j % kG, atom = f / 64, chunk = (f & 63) >> 3, e = f & 7;
-  const size_t off = (size_t)rank * kWImgBytes + atom * kAtomBytes + row * 128 + ((chunk ^ (row & 7)) << 4) + e * 2;
   *reinterpret_cast<__half *>(wimg + off) = hi;
-  *reinterpret_cast<__half *>(wimg + off + kOpBytes) = lo;
+  *reinterpret_cast<__half *>(wimg + off + lo_off) = lo;
 }
 
 // Owner cluster of global tile t under the static split [c T / ncl, (c+1) T / ncl).
@@ -181,13 +195,14 @@ struct FinParams {
   const int64_t *tile_start;  // batch + 1 (slots mode)
   const int *cstart, *cown;   // k_schedule: cluster tile split (ncl + 1), per-image owner range (2 batch)
   const float *w;
-  const double *coef;         // 3 x kDP x Kp (k_prep_w)
+  const double *coef;         // 3 x kDMax x Kp (k_prep_w)
   const float *xscale;
   float *out;                 // batch x 2KD
   double *stats_out;          // k_reduce_stats output
   double *norm2;              // batch (zeroed before k_finalize)
   unsigned *counters;         // batch (zeroed before k_finalize): last-block ticket
   int batch, K, Kp, D, ncl, mode;
+  int dpad;                   // 64 (k_stats) or 128 (k_stats_w): slot rows = [lin 0..dpad-1 | quad 0..dpad-1]
   int b_base;                 // first image of this launch (gridDim.y <= 65535 images per launch)
 };
 
@@ -209,13 +224,13 @@ __device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int 
     if (s0 >= s1) continue;
     S0 += (double)p.s0slots[(size_t)seg_slot(c, b) * p.Kp + j];
     {
-      const float *sl = p.slots + (size_t)seg_slot(c, b) * kNF * p.Kp + j;
+      const float *sl = p.slots + (size_t)seg_slot(c, b) * 2 * p.dpad * p.Kp + j;
       float v1[kFinKI], v2[kFinKI];
 #pragma unroll
       for (int i = 0; i < kFinKI; ++i) {
         const int k = kq + 8 * i;
         v1[i] = k < p.D ? __ldcs(sl + (size_t)k * p.Kp) : 0.f;          // streamed: read once
-        v2[i] = k < p.D ? __ldcs(sl + (size_t)(kDP + k) * p.Kp) : 0.f;
+        v2[i] = k < p.D ? __ldcs(sl + (size_t)(p.dpad + k) * p.Kp) : 0.f;
       }
 #pragma unroll
       for (int i = 0; i < kFinKI; ++i) { S1[i] += (double)v1[i]; S2[i] += (double)v2[i]; }
@@ -244,8 +259,9 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
   __shared__ double s_red[8];
   __shared__ int s_last;
-  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, jq = tid & 7, kr = tid >> 3;
+  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, jq = tid & 7, kr = (tid >> 3) + kDP * (int)blockIdx.z;
   const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
+  const int kb = kDP * (int)blockIdx.z, nk = min(kDP, p.D - kb);  // this block's dims [kb, kb + nk)
   const int KD = p.K * p.D;
   double ss = 0.0;
   if (4 * jq < nj) {
@@ -266,13 +282,13 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
         if ((st > ft ? st : ft) >= (en < lt ? en : lt)) continue;
         const size_t seg = (size_t)seg_slot(c, b);
         const float4 s0 = __ldcs(reinterpret_cast<const float4 *>(p.s0slots + seg * p.Kp + jb));
-        const float *sl = p.slots + seg * kNF * p.Kp + jb;
+        const float *sl = p.slots + seg * 2 * p.dpad * p.Kp + jb;
         float4 v1[kFinKR], v2[kFinKR];
 #pragma unroll
         for (int r = 0; r < kFinKR; ++r) {
           const int k = kr + 32 * r;
           v1[r] = __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)k * p.Kp));           // streamed once
-          v2[r] = __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)(kDP + k) * p.Kp));
+          v2[r] = __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)(p.dpad + k) * p.Kp));
         }
         S0[0] += (double)s0.x; S0[1] += (double)s0.y; S0[2] += (double)s0.z; S0[3] += (double)s0.w;
 #pragma unroll
@@ -325,10 +341,10 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
       if (k >= p.D) continue;
       const double *cf = p.coef + (size_t)k * p.Kp + jb;
       const double2 m01 = *reinterpret_cast<const double2 *>(cf), m23 = *reinterpret_cast<const double2 *>(cf + 2);
-      const double2 i01 = *reinterpret_cast<const double2 *>(cf + kDP * p.Kp);
-      const double2 i23 = *reinterpret_cast<const double2 *>(cf + kDP * p.Kp + 2);
-      const double2 v01 = *reinterpret_cast<const double2 *>(cf + 2 * kDP * p.Kp);
-      const double2 v23 = *reinterpret_cast<const double2 *>(cf + 2 * kDP * p.Kp + 2);
+      const double2 i01 = *reinterpret_cast<const double2 *>(cf + kDMax * p.Kp);
+      const double2 i23 = *reinterpret_cast<const double2 *>(cf + kDMax * p.Kp + 2);
+      const double2 v01 = *reinterpret_cast<const double2 *>(cf + 2 * kDMax * p.Kp);
+      const double2 v23 = *reinterpret_cast<const double2 *>(cf + 2 * kDMax * p.Kp + 2);
       const double mup[4] = {m01.x, m01.y, m23.x, m23.y}, isd[4] = {i01.x, i01.y, i23.x, i23.y},
                    ivar[4] = {v01.x, v01.y, v23.x, v23.y};
 #pragma unroll
@@ -347,17 +363,17 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
           u = (float)U;
           v = (float)V;
         }
-        sU[4 * jq + e][k] = u;
-        sV[4 * jq + e][k] = v;
+        sU[4 * jq + e][k - kb] = u;
+        sV[4 * jq + e][k - kb] = v;
       }
     }
   }
   __syncthreads();
-  float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D;
-  for (int t = tid; t < nj * p.D; t += 256) {
-    const int r = t / p.D, k = t - r * p.D;
-    o[t] = sU[r][k];
-    o[KD + t] = sV[r][k];
+  float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D + kb;
+  for (int t = tid; t < nj * nk; t += 256) {
+    const int r = t / nk, k = t - r * nk;
+    o[(size_t)r * p.D + k] = sU[r][k];
+    o[KD + (size_t)r * p.D + k] = sV[r][k];
   }
   if (p.mode == 2) return;
 #pragma unroll
@@ -370,7 +386,7 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
     if (tot != 0.0) atomicAdd(p.norm2 + b, tot);
     __threadfence();
     const unsigned ticket = atomicAdd(p.counters + b, 1u);
-    s_last = (ticket == gridDim.x - 1);
+    s_last = (ticket == gridDim.x * gridDim.z - 1);
   }
   __syncthreads();
   if (!s_last) return;
@@ -394,14 +410,14 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
 
 // a6 only: slots -> fp64 stats [N, S0, S1, S2] about c (reading A19).  Same grid as k_finalize.
 __global__ void __launch_bounds__(256) k_reduce_stats(const FinParams p) {
-  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = tid >> 5;
+  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, jj = tid & 31, kq = (tid >> 5) + kDP * (int)blockIdx.z;
   const int j = blockIdx.x * kFinJ + jj;
   if (j >= p.K) return;
   const int KD = p.K * p.D;
   double S0, S1[kFinKI], S2[kFinKI];
   slot_sums(p, b, j, kq, S0, S1, S2);
   double *st = p.stats_out + (size_t)b * (1 + (size_t)p.K * (2 * p.D + 1));
-  if (blockIdx.x == 0 && tid == 0) st[0] = (double)(p.offsets[b + 1] - p.offsets[b]);
+  if (blockIdx.x == 0 && blockIdx.z == 0 && tid == 0) st[0] = (double)(p.offsets[b + 1] - p.offsets[b]);
   if (kq == 0) st[1 + j] = S0;
 #pragma unroll
   for (int i = 0; i < kFinKI; ++i) {

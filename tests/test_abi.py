@@ -64,7 +64,7 @@ def _encode(lib, X=1, N=10, D=64, w=1, m=1, s=1, K=16, thr=0.0, flags=0, out=1):
     (dict(w=0), 1), (dict(m=0), 1), (dict(s=0), 1), (dict(X=0), 1), (dict(out=0), 1),
     (dict(K=0), 1), (dict(D=0), 1), (dict(N=-1), 1), (dict(thr=float("nan")), 1), (dict(thr=1.0), 1),
     (dict(flags=1 << 12), 1), (dict(flags=3), 1),
-    (dict(K=513), 2), (dict(D=65), 2), (dict(D=6), 2),
+    (dict(K=513), 2), (dict(D=65), 2), (dict(D=6), 2), (dict(D=132), 2),
 ])
 def test_argument_validation(lib, kw, status):
     assert _encode(lib, **kw) == status
