@@ -39,13 +39,17 @@ ISSUED_FLOP_PER_DESC = 3 * 2 * (2 * K * (2 * D))  # 3xFP16 split: 3 x (GEMM1 2K*
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--frames", type=int, default=4096, help="frames per rank (C4: 4096)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-latency", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="wall budget of the oracle sample")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="wall budget of the oracle sample")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
+                    help="c4: frame-sharded stream (default, the metric's config); c5: one 10M x 128 set, K=512, "
+                         "descriptor-sharded with an NCCL all-reduce of the fp64 statistics")
+    ap.add_argument("--c5-n", type=int, default=10_000_000, help="C5 set size (all ranks together)")
     return ap.parse_args()
 
 
@@ -66,55 +70,118 @@ def make_stream(frames: int, rank: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and throttle reasons sampled every 20 ms (NVML; nvidia-smi -lms 100 as fallback) from
+    before the warm-up to the end of the timed region; summary() keeps the samples taken between
+    mark_start() and mark_stop() (the timed region)."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+    def __init__(self, index: int, pci_bus_id: str | None = None):
+        self.index, self.bus, self.rows, self.proc, self.stop = index, pci_bus_id, [], None, threading.Event()
+        self.t0 = self.t1 = None
+        self.source = None
 
     def __enter__(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            if self.bus:
+                try:
+                    h = pynvml.nvmlDeviceGetHandleByPciBusId(self.bus)
+                except pynvml.NVMLError:
+                    h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml, self.h, self.source = pynvml, h, "nvml"
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:  # noqa: BLE001  (no NVML: fall back to nvidia-smi)
+            pass
+        try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.source = "nvidia-smi"
+            self.t = threading.Thread(target=self._smi_loop, daemon=True)
             self.t.start()
         except OSError:
             self.proc = None
         return self
 
-    def _read(self):
+    def _nvml_loop(self):
+        n = self.nvml
+        bits = [n.nvmlClocksEventReasonHwSlowdown, n.nvmlClocksEventReasonHwThermalSlowdown,
+                n.nvmlClocksEventReasonSwThermalSlowdown, n.nvmlClocksEventReasonSwPowerCap]
+        mx = n.nvmlDeviceGetMaxClockInfo(self.h, n.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
+                r = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((time.perf_counter(), float(sm), float(mx), [bool(r & b) for b in bits]))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def _smi_loop(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            r = [c.strip() for c in line.split(",")]
+            try:
+                self.rows.append((time.perf_counter(), float(r[0]), float(r[1]),
+                                  [len(r) > 4 + i and r[4 + i] == "Active" for i in range(4)]))
+            except (ValueError, IndexError):
+                pass
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_stop(self):
+        self.t1 = time.perf_counter()
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if getattr(self, "t", None):
             self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        rows = [r for r in self.rows if self.t0 is None or (self.t0 <= r[0] <= (self.t1 or r[0]))]
+        if not rows:  # timed region shorter than one sample period: use the nearest samples
+            rows = self.rows[-3:]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[3][i]})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": reasons, "samples": len(rows), "source": self.source}
+
+
+def pci_bus_id(dev):
+    try:
+        import torch
+        p = torch.cuda.get_device_properties(dev)
+        return f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def cpu_baseline_run(gmm, X, frames: int, seconds: float):
     """The fp64 oracle as it stands, on all host cores, over a bounded sample of the same stream."""
     import oracle
     threads = oracle.max_threads()
-    # ~1 s per frame per core measured on the build host; take about `seconds` of wall time
-    n = int(max(threads, min(frames, round(threads * seconds))))
+    # calibrate on one frame per thread, then size the sample to about `seconds` of wall time
+    off = np.arange(threads + 1, dtype=np.int64) * PER_FRAME
+    t = time.perf_counter()
+    oracle.encode_batched(X[:threads * PER_FRAME], off, *gmm, threshold=TAU, nthreads=threads)
+    per_round = max(1e-3, time.perf_counter() - t)
+    n = int(max(threads, min(frames, threads * round(seconds / per_round))))
     off = np.arange(n + 1, dtype=np.int64) * PER_FRAME
     t = time.perf_counter()
     oracle.encode_batched(X[:n * PER_FRAME], off, *gmm, threshold=TAU, nthreads=threads)
@@ -155,11 +222,164 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def run_c5(args, rank, world, local):
+    """C5 (BASELINE.json configs[4]): one set of args.c5_n descriptors, D=128, K=512, exact posteriors,
+    descriptor-sharded over the ranks: each rank computes the fp64 sufficient
+    statistics of its contiguous shard (fv_stats_batched), one NCCL all_reduce(SUM) of the 1+K(2D+1)
+    doubles (a8), then every rank finalises (fv_finalize).  Strong scaling (the set is fixed).  Each
+    rank draws its shard from its own seeded stream (fvgen recipe; the set's shape and distribution are
+    those of C5, its exact values depend on the world size)."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1604_03498_b200 as fv
+    from paper_1604_03498_b200 import dist as fvdist
+    cfg = fvgen.CONFIGS["C5"]
+    K5, D5, frame = cfg["K"], cfg["D"], 5000
+    lo, hi = fvdist.shard_ranges(args.c5_n // frame, world)[rank]
+    n = (hi - lo) * frame
+    gmm_np = fvgen.make_gmm(K5, D5, seed=cfg["seed_gmm"])
+    X = fvgen.make_frames(gmm_np, hi - lo, frame, seed=cfg["seed_data"] + rank * 1_000_003).reshape(n, D5)
+    gmm = fv.GMM(*gmm_np, device=dev)
+    Xd = torch.from_numpy(X).to(dev)
+    offd = torch.tensor([0, n], dtype=torch.int64, device=dev)
+    ws = fv.Workspace(device=dev)
+    ws.ensure(fv.workspace_bytes(n, 1, K5, D5))
+    fv.gmm_prepare(gmm, ws)
+    st = torch.empty(1, 1 + K5 * (2 * D5 + 1), dtype=torch.float64, device=dev)
+    out = torch.empty(1, 2 * K5 * D5, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    launches = [0]
+
+    def step():
+        fv.stats_batched(Xd, offd, gmm, ws=ws, prepared=True, out=st)
+        launches[0] = fv.last_launch_count()
+        if world > 1:
+            torch.distributed.all_reduce(st, op=torch.distributed.ReduceOp.SUM)  # a8
+        fv.finalize(st, gmm, ws=ws, prepared=True, out=out)
+        launches[0] += fv.last_launch_count()
+
+    step()
+    torch.cuda.synchronize(dev)
+    parity = None
+    if rank == 0:  # a 20k-row sample of this rank's shard through the same entry points, vs the oracle
+        import oracle
+        m = min(n, 20000)
+        s1 = fv.stats_batched(Xd[:m].contiguous(), torch.tensor([0, m], dtype=torch.int64, device=dev), gmm)
+        got = fv.finalize(s1, gmm).cpu().numpy()[0]
+        ref = oracle.encode(X[:m], *gmm_np)
+        err = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+        parity = {"sample_rows": m, "max_rel_l2": err, "tolerance": 1e-4}
+        if err > 1e-4:
+            raise SystemExit(f"parity failure before timing: {err}")
+    clk = ClockSampler(local, pci_bus_id(dev)).__enter__()
+    for _ in range(max(3, args.warmup)):
+        step()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in kev:
+        a.record(stream)
+        b.record(stream)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clk.mark_start()
+    try:
+        t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            fv.profile_events(*kev[i])
+            step()
+        t_stop.record(stream)
+        fv.profile_events(None, None)
+        torch.cuda.synchronize(dev)
+    finally:
+        clk.mark_stop()
+        clk.__exit__(None, None, None)
+    if world > 1:
+        torch.distributed.barrier()
+    total_ms = t_start.elapsed_time(t_stop)
+    kms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    n_all = (args.c5_n // frame) * frame
+    value = n_all * args.steps / (total_ms * 1e-3)
+
+    # end to end: pinned host shard -> device, statistics, all-reduce, finalize, FV -> host (host clock)
+    e2e = None
+    if args.e2e_steps > 0:
+        Xh = torch.from_numpy(X).pin_memory()
+        outh = torch.empty(2 * K5 * D5, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            step()
+            outh.copy_(out[0], non_blocking=True)
+            torch.cuda.synchronize(dev)
+
+        e2e_step()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": n_all * args.e2e_steps / el, "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 4),
+               "d2h_bytes_per_step": int(outh.numel() * 4),
+               "note": "pinned host shard -> device, stats, all-reduce, finalize, FV -> pinned host; host clock"}
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    flop = 4 * K5 * (2 * D5 + 1)
+    peak_tf = load_peaks().get("bf16_tflops_sustained", 1400.0)
+    achieved = flop * n / (kms * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+        "precision": "3xFP16 split operands on tcgen05, fp32 accumulate, fp64 statistics/finalize",
+        "config": {"workload": f"C5 single set: {n_all} descriptors x {D5}, K={K5}, exact posteriors, "
+                               f"descriptor-sharded x{world} + NCCL all_reduce of {st.numel()} fp64 statistics",
+                   "K": K5, "D": D5, "descriptors": n_all, "threshold": 0.0,
+                   "parallelism": f"descriptor-sharded x{world}, all_reduce(SUM) of [N,S0,S1,S2]",
+                   "l2": f"inputs {n * D5 * 4 / 1e9:.2f} GB per rank > 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tf, "traffic": None, "kernel": "k_stats_w", "kernel_ms": kms,
+                     "kernel_share_of_step": kms / (total_ms / args.steps), "flop_per_desc": flop,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kind::f16 = bf16 rate)"},
+        "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches[0] * args.steps, "parity": parity,
+        "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.workload == "c5":
+        run_c5(args, rank, world, local)
         return
     import torch
     torch.cuda.set_device(local)
@@ -199,6 +419,7 @@ def main():
         if max(errs) > 1e-4:
             raise SystemExit(f"parity failure before timing: {errs}")
 
+    clk = ClockSampler(local, pci_bus_id(dev)).__enter__()  # sampling from before the warm-up
     for _ in range(max(3, args.warmup)):
         step()
     launches_per_step = fv.last_launch_count()
@@ -210,7 +431,8 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    clk.mark_start()
+    try:
         t_start = torch.cuda.Event(enable_timing=True)
         t_stop = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
@@ -222,6 +444,9 @@ def main():
         t_stop.record(stream)
         fv.profile_events(None, None)
         torch.cuda.synchronize(dev)
+    finally:
+        clk.mark_stop()
+        clk.__exit__(None, None, None)
     if world > 1:
         torch.distributed.barrier()
     total_ms = t_start.elapsed_time(t_stop)
@@ -305,13 +530,7 @@ def main():
             torch.distributed.destroy_process_group()
         return
 
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except OSError:
-        pass
-    peak_tf = peaks.get("bf16_tflops_sustained", 1400.0)  # kind::f16 (fp16) runs at the bf16 rate
+    peak_tf = load_peaks().get("bf16_tflops_sustained", 1400.0)  # kind::f16 (fp16) runs at the bf16 rate
     kms = statistics.mean(kstats_ms)
     achieved = FLOP_PER_DESC * n_total / (kms * 1e-3) / 1e12
     traffic = None
