@@ -41,46 +41,72 @@ with open(os.path.join(out_dir, f"{tag}_launch_list.md"), "w") as f:
     for name, val in order:
         f.write(f"- {name}: {val:.1f} us\n")
 
-# ---- k_stats full capture: headline metrics
-rep = os.path.join(g, f"{tag}_kstats.ncu-rep")
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-r = list(csv.reader(raw.splitlines()))
-h, u, v = r[0], r[1], r[2]
-want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+# ---- full captures: headline metrics, pipe shares, stall reasons
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
-        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
-        "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "launch__cluster_size",
-        "sm__cycles_elapsed.avg", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
-vals = {}
-for w in want:
-    if w in h:
-        i = h.index(w)
-        vals[w] = (v[i], u[i])
-dram = None
-try:
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "smsp__mem_tensor_reads_op_ldt.sum.pct_of_peak_sustained_elapsed",
+        "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "launch__cluster_size", "sm__cycles_elapsed.avg", "sm__warps_active.avg.pct_of_peak_sustained_active"]
+
+
+def capture(name, title, cmd):
+    rep = os.path.join(g, f"{tag}_{name}.ncu-rep")
+    if not os.path.exists(rep):
+        return None
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(raw.splitlines()))
+    h, u, v = r[0], r[1], r[2]
+    vals = {w: (v[h.index(w)], u[h.index(w)]) for w in WANT if w in h}
+    stalls = []
+    for i, nm in enumerate(h):
+        if nm.startswith("smsp__pcsamp_warps_issue_stalled_") and not nm.endswith("not_issued"):
+            try:
+                stalls.append((float(v[i]), nm[len("smsp__pcsamp_warps_issue_stalled_"):]))
+            except ValueError:
+                pass
+    tot = sum(x for x, _ in stalls) or 1.0
+
     def tobytes(val, unit):
         return float(val.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-    dram = tobytes(*vals["dram__bytes_read.sum"]) + tobytes(*vals["dram__bytes_write.sum"])
-except KeyError:
-    pass
-with open(os.path.join(out_dir, f"{tag}_kstats_ncu.md"), "w") as f:
-    f.write(f"# {tag}: k_stats, ncu --set full --clock-control none (one launch, C4 workload)\n\n")
-    f.write("Command: `ncu --set full --clock-control none --import-source on -k regex:k_stats -s 3 -c 1 "
-            "python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-latency --cpu-seconds 0`\n\n")
-    f.write("| metric | value | unit |\n|---|---|---|\n")
-    for w in want:
-        if w in vals:
-            f.write(f"| {w} | {vals[w][0]} | {vals[w][1]} |\n")
-    if dram is not None:
-        f.write(f"\nDRAM traffic per launch: {dram/1e9:.3f} GB (read + write).\n")
+    dram = None
+    if "dram__bytes_read.sum" in vals and "dram__bytes_write.sum" in vals:
+        dram = tobytes(*vals["dram__bytes_read.sum"]) + tobytes(*vals["dram__bytes_write.sum"])
+    with open(os.path.join(out_dir, f"{tag}_{name}_ncu.md"), "w") as f:
+        f.write(f"# {tag}: {title}, ncu --set full --clock-control none (one launch)\n\nCommand: `{cmd}`\n\n")
+        f.write("| metric | value | unit |\n|---|---|---|\n")
+        for w in WANT:
+            if w in vals:
+                f.write(f"| {w} | {vals[w][0]} | {vals[w][1]} |\n")
+        if dram is not None:
+            f.write(f"\nDRAM traffic per launch: {dram/1e9:.3f} GB (read + write).\n")
+        f.write("\nWarp stall reasons (share of PC samples):\n\n")
+        for x, nm in sorted(stalls, reverse=True)[:10]:
+            f.write(f"- {nm}: {100*x/tot:.1f}%\n")
+    return dram
+
+
+NC = "ncu --set full --clock-control none --import-source on"
+dram = capture("kstats", "k_stats (narrow, D=64) on C4",
+               f"{NC} -k regex:k_stats -s 3 -c 1 python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-latency --cpu-seconds 0")
+capture("finalize", "k_finalize on C4",
+        f"{NC} -k regex:k_finalize -s 3 -c 1 python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-latency --cpu-seconds 0")
+capture("kstats_w", "k_stats_w (wide, D=128, K=512) on a 2M-row C5 set",
+        f"{NC} -k regex:k_stats_w -s 3 -c 1 python bench.py --workload c5 --c5-n 2000000 --steps 1 --warmup 3 --e2e-steps 0")
 n_total = 4096 * 5000
 with open(os.path.join(out_dir, "kstats_traffic.json"), "w") as f:
     json.dump({"tag": tag, "n_total": n_total, "dram_bytes_per_launch": dram,
                "source": f"profiles/{tag}_kstats_ncu.md"}, f, indent=1)
 print(open(os.path.join(out_dir, f"{tag}_launch_list.md")).read()[:1500])
-print(open(os.path.join(out_dir, f"{tag}_kstats_ncu.md")).read())
+for nm in ("kstats", "finalize", "kstats_w"):
+    pth = os.path.join(out_dir, f"{tag}_{nm}_ncu.md")
+    if os.path.exists(pth):
+        print(open(pth).read())

@@ -1,7 +1,8 @@
 #!/usr/bin/env bash
-# Run on the GPU box (gpurun): launch list of the bench command + one ncu --set full capture of
-# k_stats on the full C4 workload.  Outputs land in gpurun_out/ (scratch); tools/ncu_summary.py
-# turns them into the committed profiles/ summaries.
+# Run on the GPU box (gpurun): launch list of the bench command + ncu --set full captures of the
+# stats kernel on the full C4 workload, of k_finalize (C4), and of the wide stats kernel (C5 shape,
+# 2M rows).  Outputs land in gpurun_out/ (scratch); tools/ncu_summary.py turns them into the
+# committed profiles/ summaries.
 set -u
 TAG=${1:-r01}
 python __graft_entry__.py
@@ -13,3 +14,11 @@ timeout -s KILL 1200 ncu --set full --clock-control none --import-source on -k r
   -o gpurun_out/${TAG}_kstats python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-latency --cpu-seconds 0 \
   > gpurun_out/${TAG}_kstats.log 2>&1
 tail -2 gpurun_out/${TAG}_kstats.log
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_finalize -s 3 -c 1 \
+  -o gpurun_out/${TAG}_finalize python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-latency --cpu-seconds 0 \
+  > gpurun_out/${TAG}_finalize.log 2>&1
+tail -1 gpurun_out/${TAG}_finalize.log
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_stats_w -s 3 -c 1 \
+  -o gpurun_out/${TAG}_kstats_w python bench.py --workload c5 --c5-n 2000000 --steps 1 --warmup 3 --e2e-steps 0 \
+  > gpurun_out/${TAG}_kstats_w.log 2>&1
+tail -1 gpurun_out/${TAG}_kstats_w.log
