@@ -48,9 +48,9 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Tile family: D <= 64 -> k_stats (128 Gaussians per CTA, cluster <= 4); 64 < D <= 128 -> k_stats_w
 // (64 Gaussians per CTA, cluster <= 8).  K <= 512 for both.
-bool is_wide(int D) { return D > kDP; }
-int gauss_per_cta(int D) { return is_wide(D) ? kGW : kG; }
-int cluster_size(int K, int D) { return (K + gauss_per_cta(D) - 1) / gauss_per_cta(D); }
+bool is_wide(int K, int D) { return D > kDP || K > kG * kMaxC2; }
+int gauss_per_cta(int K, int D) { return is_wide(K, D) ? kGW : kG; }
+int cluster_size(int K, int D) { return (K + gauss_per_cta(K, D) - 1) / gauss_per_cta(K, D); }
 
 // Persistent grid: the number of co-resident clusters of the stats kernel on the current device.
 int num_clusters(int C, bool wide) {
@@ -101,9 +101,9 @@ struct Layout {
 
 bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout &L) {
   L.C = cluster_size(K, D);
-  L.Kp = L.C * gauss_per_cta(D);
-  L.dpad = is_wide(D) ? kDMax : kDP;
-  L.ncl = num_clusters(L.C, is_wide(D));
+  L.Kp = L.C * gauss_per_cta(K, D);
+  L.dpad = is_wide(K, D) ? kDMax : kDP;
+  L.ncl = num_clusters(L.C, is_wide(K, D));
   if (L.ncl <= 0) return false;
   // one slot per (cluster, image) segment, index cid + b (seg_slot, fv_common.cuh)
   L.n_total = n_total;
@@ -121,7 +121,7 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.cstart = o;   o = align_up(o + (size_t)(L.ncl + 1) * 4, 256);
   L.cown = o;     o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 8, 256);
   L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 12, 1024);  // double norm2[] + uint counters[]
-  L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * L.Kp * 4, 1024);
+  L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * 4 * L.Kp * 4, 1024);
   L.slots = o;    o = align_up(o + (size_t)L.nslots * 2 * L.dpad * L.Kp * 4, 1024);
   L.hx = L.hoff = L.hout = 0;
   if (host_io) {
@@ -136,7 +136,7 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
 fv_status check_gmm_args(int K, int D, const float *w, const float *mu, const float *sg, unsigned flags) {
   if (!w || !mu || !sg) return fail(FV_ERR_ARG, "null GMM pointer");
   if (K < 1 || D < 1) return fail(FV_ERR_ARG, "K=%d and D=%d must be >= 1", K, D);
-  if (K > kG * kMaxC2) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kG * kMaxC2);  // 512 for both tile families
+  if (K > kMaxK) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kMaxK);
   if (D > kDMax) return fail(FV_ERR_UNSUPPORTED, "D=%d > %d", D, kDMax);
   if (D % 4 != 0) return fail(FV_ERR_UNSUPPORTED, "D=%d is not a multiple of 4 (pad, reading A13)", D);
   const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED;
@@ -173,7 +173,7 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
   k_prep_shift<<<1, 256, 0, st>>>(w, mu, sg, K, D, L.Kp, sd, (double *)at(ws, L.cshift), (float *)at(ws, L.xshift),
                                   (float *)at(ws, L.xscale), (float *)at(ws, L.bias), (double *)at(ws, L.bscratch));
   k_prep_w<<<L.Kp, 2 * L.dpad, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
-                                 at(ws, L.wimg), (double *)at(ws, L.coef), is_wide(D) ? 1 : 0);
+                                 at(ws, L.wimg), (double *)at(ws, L.coef), is_wide(K, D) ? 1 : 0);
   g_launches += 2;
   return cuda_check("k_prep");
 }
@@ -234,13 +234,13 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   attr[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3(L.C * L.ncl, 1, 1);
   cfg.blockDim = dim3(kThreads2, 1, 1);
-  cfg.dynamicSmemBytes = is_wide(D) ? kSmemWBytes : kSmem2Bytes;
+  cfg.dynamicSmemBytes = is_wide(K, D) ? kSmemWBytes : kSmem2Bytes;
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (g_prof_start) cudaEventRecord(g_prof_start, st);
   cudaError_t e;
-  if (!is_wide(D)) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false>, tmap, p);
+  if (!is_wide(K, D)) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false>, tmap, p);
   else e = (D == kDMax) ? cudaLaunchKernelEx(&cfg, k_stats_w<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false>, tmap, p);
   if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
   g_launches += 1;
@@ -329,7 +329,7 @@ extern "C" {
 size_t fv_workspace_bytes(int64_t n_total, int batch, int K, int D, unsigned flags) {
   (void)flags;
   Layout L;
-  if (K < 1 || K > kG * kMaxC2 || batch < 0 || n_total < 0) return 0;
+  if (K < 1 || K > kMaxK || batch < 0 || n_total < 0) return 0;
   if (!make_layout(n_total, batch, K, D, false, L)) return 0;
   return L.total;
 }
@@ -337,7 +337,7 @@ size_t fv_workspace_bytes(int64_t n_total, int batch, int K, int D, unsigned fla
 size_t fv_workspace_bytes_host(int64_t n_total, int batch, int K, int D, unsigned flags) {
   (void)flags;
   Layout L;
-  if (K < 1 || K > kG * kMaxC2 || batch < 0 || n_total < 0) return 0;
+  if (K < 1 || K > kMaxK || batch < 0 || n_total < 0) return 0;
   if (!make_layout(n_total, batch, K, D, true, L)) return 0;
   return L.total;
 }

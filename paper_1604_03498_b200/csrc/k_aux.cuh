@@ -189,7 +189,7 @@ __global__ void k_schedule(const int64_t *offsets, int64_t *off1, int64_t n_sing
 
 struct FinParams {
   const float *slots;         // segment slots from k_stats: (ncl + batch) x kNF x Kp (nullptr: stats)
-  const float *s0slots;       // (ncl + batch) x Kp
+  const float *s0slots;       // (ncl + batch) x 4 row groups x Kp
   const double *stats;        // batch x (1 + K(2D+1)) (nullptr when reading slots)
   const int64_t *offsets;     // batch + 1 (slots mode)
   const int64_t *tile_start;  // batch + 1 (slots mode)
@@ -222,7 +222,8 @@ __device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int 
     const int st = p.cstart[c], en = p.cstart[c + 1];
     const int s0 = st > ft ? st : ft, s1 = en < lt ? en : lt;
     if (s0 >= s1) continue;
-    S0 += (double)p.s0slots[(size_t)seg_slot(c, b) * p.Kp + j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) S0 += (double)p.s0slots[((size_t)seg_slot(c, b) * 4 + q) * p.Kp + j];  // row groups
     {
       const float *sl = p.slots + (size_t)seg_slot(c, b) * 2 * p.dpad * p.Kp + j;
       float v1[kFinKI], v2[kFinKI];
@@ -281,7 +282,13 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
         const int st = p.cstart[c], en = p.cstart[c + 1];
         if ((st > ft ? st : ft) >= (en < lt ? en : lt)) continue;
         const size_t seg = (size_t)seg_slot(c, b);
-        const float4 s0 = __ldcs(reinterpret_cast<const float4 *>(p.s0slots + seg * p.Kp + jb));
+        float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        double s0d[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // the 4 row-group partials, fixed order
+          s0 = __ldcs(reinterpret_cast<const float4 *>(p.s0slots + (seg * 4 + q) * p.Kp + jb));
+          s0d[0] += (double)s0.x; s0d[1] += (double)s0.y; s0d[2] += (double)s0.z; s0d[3] += (double)s0.w;
+        }
         const float *sl = p.slots + seg * 2 * p.dpad * p.Kp + jb;
         float4 v1[kFinKR], v2[kFinKR];
 #pragma unroll
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
           v1[r] = __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)k * p.Kp));           // streamed once
           v2[r] = __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)(p.dpad + k) * p.Kp));
         }
-        S0[0] += (double)s0.x; S0[1] += (double)s0.y; S0[2] += (double)s0.z; S0[3] += (double)s0.w;
+        S0[0] += s0d[0]; S0[1] += s0d[1]; S0[2] += s0d[2]; S0[3] += s0d[3];
 #pragma unroll
         for (int r = 0; r < kFinKR; ++r) {
           S1[r][0] += (double)v1[r].x; S1[r][1] += (double)v1[r].y; S1[r][2] += (double)v1[r].z; S1[r][3] += (double)v1[r].w;

@@ -40,7 +40,8 @@ namespace gpufv {
 constexpr int kWarpsWork = 16;
 constexpr int kWarpMma = kWarpsWork, kWarpTma = kWarpsWork + 1;
 constexpr int kThreads2 = (kWarpTma + 1) * 32;  // 576
-constexpr int kMaxC2 = 4;                        // K <= 512 in this kernel
+constexpr int kMaxC2 = 2;                        // K <= 256 in this kernel (larger K: k_stats_w)
+constexpr int kMaxK = 512;                       // both tile families
 
 // per-tile metadata published by the TMA thread (ring of 4: slot t % 4 stays valid well past tile t)
 struct TileMeta {
@@ -56,9 +57,8 @@ constexpr int kXBoxBytes = 128 * 128;                // 32 floats x 128 rows
 constexpr int kS2Bias = kS2X + kXBoxBytes;           // float[128]
 constexpr int kS2Cs = kS2Bias + kG * 4;              // float[64]  -c_k 2^e_k
 constexpr int kS2Sc = kS2Cs + kDP * 4;               // float[64]  2^e_k
-constexpr int kS2Red = kS2Sc + kDP * 4;              // float2[2][4][128] (max, sum) per column quarter, by tile parity
-constexpr int kS2Xchg = kS2Red + 2 * 4 * kTileM * 8; // float2[2][kMaxC2][128]
-constexpr int kS2Meta = kS2Xchg + 2 * kMaxC2 * kTileM * 8;  // TileMeta[4]
+constexpr int kS2Xchg = kS2Sc + kDP * 4;             // float2[2 parity][kMaxC2 ranks][4 quarters][128 rows] (m, s)
+constexpr int kS2Meta = kS2Xchg + 2 * kMaxC2 * 4 * kTileM * 8;  // TileMeta[4]
 constexpr int kS2Bar = kS2Meta + 128;                // uint64 barriers
 constexpr int kNumBars = 16;
 constexpr int kS2Tmem = kS2Bar + kNumBars * 8;
@@ -75,8 +75,7 @@ enum : int {
 constexpr uint32_t kTZr = 0, kTL = 256, kTS = 384;
 
 // named barriers (0 = __syncthreads)
-constexpr uint32_t kBarLane0 = 1;  // 1..4: the 4 WORK warps of a TMEM lane group (128 threads)
-constexpr uint32_t kBarWork = 5;   // all 16 WORK warps (512 threads)
+constexpr uint32_t kBarLane0 = 1;  // 1..4: the 4 WORK warps of a TMEM lane group (k_stats_w's quarter combine)
 
 struct Stats2Params {
   const float *X;             // n_total x D (also behind the tensor map; used for L2 prefetch)
@@ -221,11 +220,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   float *s_bias = reinterpret_cast<float *>(smem + kS2Bias);
   float *s_ncs = reinterpret_cast<float *>(smem + kS2Cs);
   float *s_sc = reinterpret_cast<float *>(smem + kS2Sc);
-  float2 *s_red = reinterpret_cast<float2 *>(smem + kS2Red);
   float2 *s_xchg = reinterpret_cast<float2 *>(smem + kS2Xchg);
-  // S0 segment flush scratch float[4][128]: aliases the (m, s) buffer of the NEXT tile's parity, which
-  // no warp reads or writes between the two kBarWork barriers of the flush
-  float *s_s0_base = reinterpret_cast<float *>(smem + kS2Red);
   TileMeta *s_meta = reinterpret_cast<TileMeta *>(smem + kS2Meta);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kS2Bar);
   uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + kS2Tmem);
@@ -468,7 +463,18 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         }
         return sacc.x + sacc.y;
       };
-      float2 *red = s_red + (i & 1) * (4 * kTileM);  // parity buffer: tile i+1 never overwrites tile i's
+      // (m_h, s_h) of this warp's quarter -> slot [rank][h][row] of every CTA of the cluster (itself
+      // included) by st.async on the parity buffer's mbarrier: one wait then gives each row the 4C
+      // quarter pairs (no named barrier; parity double buffer, see DESIGN.md §6 for why no warp can
+      // overwrite a buffer still being read)
+      const int par = i & 1;
+      float2 *xb = s_xchg + par * (kMaxC2 * 4 * kTileM);
+      auto send = [&](float ssum) {
+        if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[B_XCHG0 + par], C * 4 * kTileM * 8);
+        const uint32_t my = smem_u32(&xb[(rank * 4 + h) * kTileM + row]);
+        const uint32_t mybar = smem_u32(&bars[B_XCHG0 + par]);
+        for (uint32_t r2 = 0; r2 < C; ++r2) st_async_v2f32(mapa_shared(my, r2), m, ssum, mapa_shared(mybar, r2));
+      };
       if (i + 1 < n) {
         // Zr(i+1) box 0 (resident since the previous tile) in the same basic block as the exp loop:
         // its FMA/ALU work fills the issue slots the MUFU-bound exponentials leave idle
@@ -476,56 +482,34 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         const int nr1 = s_meta[(i + 1) & 3].nrows;
         const float ssum = exp_local();
         zr_box<true>(xbox, row, 0, h, D, row < nr1, s_sc, s_ncs, tmem + kTZr + 128 * ((i + 1) & 1) + lane_base);
-        red[h * kTileM + row] = make_float2(m, ssum);
+        send(ssum);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[B_XEMPTY0]);  // box 1 streams in behind the combine below
+        if (lane == 0) mbar_arrive(&bars[B_XEMPTY0]);  // box 1 streams in behind the exchange below
       } else {
-        red[h * kTileM + row] = make_float2(m, exp_local());
+        send(exp_local());
       }
       TRW(4);
-      named_bar_sync(kBarLane0 + q, 128);
-      TRW(5);
-      float M, S;
+      mbar_wait(&bars[B_XCHG0 + par], (i >> 1) & 1);
+      TRW(12);
+      float M = -3.0e38f, S = 0.f;
       {
-        const float2 r0 = red[row], r1 = red[kTileM + row], r2 = red[2 * kTileM + row], r3 = red[3 * kTileM + row];
-        M = fmaxf(fmaxf(r0.x, r1.x), fmaxf(r2.x, r3.x));
-        S = (r0.y * ex2_approx(r0.x - M) + r1.y * ex2_approx(r1.x - M)) +
-            (r2.y * ex2_approx(r2.x - M) + r3.y * ex2_approx(r3.x - M));
-      }
-      if (C > 1) {
-        const int par = i & 1;
-        float2 *xb = s_xchg + par * (kMaxC2 * kTileM);
-        if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[B_XCHG0 + par], (C - 1) * kTileM * 8);
-        if (h == 0) {
-          const uint32_t my = smem_u32(&xb[rank * kTileM + row]);
-          const uint32_t mybar = smem_u32(&bars[B_XCHG0 + par]);
-          for (uint32_t r2 = 0; r2 < C; ++r2)
-            if (r2 != rank) st_async_v2f32(mapa_shared(my, r2), M, S, mapa_shared(mybar, r2));
-        }
-        TRW(13);
-        if (i + 1 < n) conv_box(i + 1, 1);  // fills the partner-exchange latency
-        mbar_wait(&bars[B_XCHG0 + par], (i >> 1) & 1);
-        TRW(12);
-        float2 o[kMaxC2];
-        float Mg = M;
+        float2 o[kMaxC2 * 4];
 #pragma unroll
-        for (int r2 = 0; r2 < kMaxC2; ++r2) {
-          o[r2] = make_float2(-3.0e38f, 0.f);
-          if (r2 < (int)C && r2 != (int)rank) { o[r2] = xb[r2 * kTileM + row]; Mg = fmaxf(Mg, o[r2].x); }
+        for (int e = 0; e < kMaxC2 * 4; ++e) {
+          o[e] = make_float2(-3.0e38f, 0.f);
+          if (e < (int)C * 4) { o[e] = xb[e * kTileM + row]; M = fmaxf(M, o[e].x); }
         }
-        float Sg = S * ex2_approx(M - Mg);
 #pragma unroll
-        for (int r2 = 0; r2 < kMaxC2; ++r2) Sg += o[r2].y * ex2_approx(o[r2].x - Mg);
-        M = Mg;
-        S = Sg;
-      } else if (i + 1 < n) {
-        conv_box(i + 1, 1);
+        for (int e = 0; e < kMaxC2 * 4; ++e) S += o[e].y * ex2_approx(o[e].x - M);
       }
       // this quarter's gamma_ij = e_ij 2^(m_h - M) / S; P = gamma 2^14
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
       if (row >= mt.nrows) alpha_p = 0.f;
       TRW(6);
+      // Zr(i+1) box 1: its TMA load started when box 0 was released above (a single 16 KB stage)
+      if (i + 1 < n) conv_box(i + 1, 1);
+      TRW(13);
 
       // ---- GEMM2(i-1) done: S' chunk complete (fold), Z and P free
       if (i >= 1) {
@@ -571,17 +555,11 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[B_P_FULL]);
       TRW(9);
-      if (mt.flags & 1) {  // segment end: S0 (units of 2^14 gamma) -> s0 slot (cid + b)
-        float *s_s0 = s_s0_base + ((i + 1) & 1) * (4 * kTileM * 2);
+      if (mt.flags & 1) {  // segment end: S0 (units of 2^14 gamma), this warp's 32 rows -> partial slot q
         warp_transpose_reduce32(s0acc, lane);
-        s_s0[q * kG + 32 * h + lane] = s0acc[0];
+        p.s0slots[((size_t)seg_slot(cid, mt.b) * 4 + q) * p.Kp + rank * kG + 32 * h + lane] = s0acc[0];
 #pragma unroll
         for (int j = 0; j < 32; ++j) s0acc[j] = 0.f;
-        named_bar_sync(kBarWork, kWarpsWork * 32);
-        if (tid < kG)
-          p.s0slots[(size_t)seg_slot(cid, mt.b) * p.Kp + rank * kG + tid] =
-              (s_s0[tid] + s_s0[kG + tid]) + (s_s0[2 * kG + tid] + s_s0[3 * kG + tid]);
-        named_bar_sync(kBarWork, kWarpsWork * 32);
       }
       prev_b = mt.b;
       prev_fold = (mt.flags & 4) != 0;

@@ -67,7 +67,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
   float *s_sc = reinterpret_cast<float *>(smem + kWSc);
   float2 *s_red = reinterpret_cast<float2 *>(smem + kWRed);
   float2 *s_xchg = reinterpret_cast<float2 *>(smem + kWXchg);
-  float *s_s0_base = reinterpret_cast<float *>(smem + kWRed);  // aliases the next tile's (m, s) parity buffer
   TileMeta *s_meta = reinterpret_cast<TileMeta *>(smem + kWMeta);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kWBar);
   uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + kWTmem);
@@ -393,20 +392,14 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[W_ZB_FULL]);
       if (i + 1 < n) conv_half(i + 1, 1);
-      if (mt.flags & 1) {  // segment end: S0 (units of 2^14 gamma) -> s0 slot
-        float *s_s0 = s_s0_base + ((i + 1) & 1) * (4 * kTileM * 2);
+      if (mt.flags & 1) {  // segment end: S0 (units of 2^14 gamma), this warp's 32 rows -> partial slot q
         float t32[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) t32[j] = j < 16 ? s0acc[j] : 0.f;
         warp_transpose_reduce32(t32, lane);  // lane l < 16: column l summed over the warp's rows
-        if (lane < 16) s_s0[q * kGW + 16 * h + lane] = t32[0];
+        if (lane < 16) p.s0slots[((size_t)seg_slot(cid, mt.b) * 4 + q) * p.Kp + rank * kGW + 16 * h + lane] = t32[0];
 #pragma unroll
         for (int j = 0; j < 16; ++j) s0acc[j] = 0.f;
-        named_bar_sync(kBarWork, kWarpsWork * 32);
-        if (tid < kGW)
-          p.s0slots[(size_t)seg_slot(cid, mt.b) * p.Kp + rank * kGW + tid] =
-              (s_s0[tid] + s_s0[kGW + tid]) + (s_s0[2 * kGW + tid] + s_s0[3 * kGW + tid]);
-        named_bar_sync(kBarWork, kWarpsWork * 32);
       }
       prev_b = mt.b;
       prev_fold = (mt.flags & 4) != 0;
