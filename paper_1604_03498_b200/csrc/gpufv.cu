@@ -48,6 +48,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Tile family: D <= 64 -> k_stats (128 Gaussians per CTA, cluster <= 4); 64 < D <= 128 -> k_stats_w
 // (64 Gaussians per CTA, cluster <= 8).  K <= 512 for both.
+constexpr int kMinTilesPerCluster = 4;
 bool is_wide(int K, int D) { return D > kDP || K > kG * kMaxC2; }
 int gauss_per_cta(int K, int D) { return is_wide(K, D) ? kGW : kG; }
 int cluster_size(int K, int D) { return (K + gauss_per_cta(K, D) - 1) / gauss_per_cta(K, D); }
@@ -105,6 +106,10 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.dpad = is_wide(K, D) ? kDMax : kDP;
   L.ncl = num_clusters(L.C, is_wide(K, D));
   if (L.ncl <= 0) return false;
+  // small launches (one frame): at least kMinTilesPerCluster tiles per cluster, so an image is split
+  // into fewer (cluster) segments for the finalize to combine; tiles <= n_total/128 + batch
+  const int64_t tmax = n_total / kTileM + batch;
+  if (tmax > 0) L.ncl = (int)std::min<int64_t>(L.ncl, std::max<int64_t>(1, (tmax + kMinTilesPerCluster - 1) / kMinTilesPerCluster));
   // one slot per (cluster, image) segment, index cid + b (seg_slot, fv_common.cuh)
   L.n_total = n_total;
   L.nslots = (int64_t)L.ncl + batch + 1;

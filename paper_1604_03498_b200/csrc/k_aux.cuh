@@ -278,31 +278,56 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
       N = (double)(p.offsets[b + 1] - p.offsets[b]);
       const int ft = (int)p.tile_start[b], lt = (int)p.tile_start[b + 1];
       const int clo = p.cown[2 * b], chi = p.cown[2 * b + 1];
-      for (int c = clo; c <= chi; ++c) {
-        const int st = p.cstart[c], en = p.cstart[c + 1];
-        if ((st > ft ? st : ft) >= (en < lt ? en : lt)) continue;
-        const size_t seg = (size_t)seg_slot(c, b);
-        float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f);
-        double s0d[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {  // the 4 row-group partials, fixed order
-          s0 = __ldcs(reinterpret_cast<const float4 *>(p.s0slots + (seg * 4 + q) * p.Kp + jb));
-          s0d[0] += (double)s0.x; s0d[1] += (double)s0.y; s0d[2] += (double)s0.z; s0d[3] += (double)s0.w;
+      // segments are taken two at a time with all their loads issued before either is accumulated
+      // (a single image spread over many clusters would otherwise cost one L2 round trip per segment);
+      // accumulation stays in ascending cluster order
+      auto next_seg = [&](int &c) {  // next non-empty segment at or after c (-1: none); advances c
+        for (; c <= chi; ++c) {
+          const int st = p.cstart[c], en = p.cstart[c + 1];
+          if ((st > ft ? st : ft) < (en < lt ? en : lt)) return c++;
         }
-        const float *sl = p.slots + seg * 2 * p.dpad * p.Kp + jb;
-        float4 v1[kFinKR], v2[kFinKR];
+        return -1;
+      };
+      for (int c = clo; c <= chi;) {  // S0: 4 row-group partials per segment
+        const int sa = next_seg(c), sb = next_seg(c);
+        float4 s0[2][4];
 #pragma unroll
-        for (int r = 0; r < kFinKR; ++r) {
-          const int k = kr + 32 * r;
-          v1[r] = __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)k * p.Kp));           // streamed once
-          v2[r] = __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)(p.dpad + k) * p.Kp));
-        }
-        S0[0] += s0d[0]; S0[1] += s0d[1]; S0[2] += s0d[2]; S0[3] += s0d[3];
+        for (int u = 0; u < 2; ++u) {
+          const int sg = u == 0 ? sa : sb;
 #pragma unroll
-        for (int r = 0; r < kFinKR; ++r) {
-          S1[r][0] += (double)v1[r].x; S1[r][1] += (double)v1[r].y; S1[r][2] += (double)v1[r].z; S1[r][3] += (double)v1[r].w;
-          S2[r][0] += (double)v2[r].x; S2[r][1] += (double)v2[r].y; S2[r][2] += (double)v2[r].z; S2[r][3] += (double)v2[r].w;
+          for (int q = 0; q < 4; ++q)
+            s0[u][q] = sg < 0 ? make_float4(0.f, 0.f, 0.f, 0.f)
+                              : __ldcs(reinterpret_cast<const float4 *>(p.s0slots + ((size_t)seg_slot(sg, b) * 4 + q) * p.Kp + jb));
         }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            S0[0] += (double)s0[u][q].x; S0[1] += (double)s0[u][q].y; S0[2] += (double)s0[u][q].z; S0[3] += (double)s0[u][q].w;
+          }
+      }
+      for (int c = clo; c <= chi;) {  // S1, S2
+        const int sa = next_seg(c), sb = next_seg(c);
+        float4 v1[2][kFinKR], v2[2][kFinKR];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int sg = u == 0 ? sa : sb;
+          const float *sl = p.slots + (size_t)seg_slot(sg < 0 ? 0 : sg, b) * 2 * p.dpad * p.Kp + jb;
+#pragma unroll
+          for (int r = 0; r < kFinKR; ++r) {
+            const int k = kr + 32 * r;
+            v1[u][r] = sg < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)k * p.Kp));
+            v2[u][r] = sg < 0 ? make_float4(0.f, 0.f, 0.f, 0.f)
+                              : __ldcs(reinterpret_cast<const float4 *>(sl + (size_t)(p.dpad + k) * p.Kp));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int r = 0; r < kFinKR; ++r) {
+            S1[r][0] += (double)v1[u][r].x; S1[r][1] += (double)v1[u][r].y; S1[r][2] += (double)v1[u][r].z; S1[r][3] += (double)v1[u][r].w;
+            S2[r][0] += (double)v2[u][r].x; S2[r][1] += (double)v2[u][r].y; S2[r][2] += (double)v2[u][r].z; S2[r][3] += (double)v2[u][r].w;
+          }
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e) S0[e] *= 1.0 / (double)kPScale;  // S0 was accumulated from P = gamma 2^14

@@ -68,7 +68,7 @@ static_assert(kSmem2Bytes <= 232448, "shared memory budget");
 // barrier slots
 enum : int {
   B_XFULL0 = 0, B_XFULL1, B_XEMPTY0, B_XEMPTY1, B_ZR_FULL, B_G1_DONE, B_G2_DONE,
-  B_L_EMPTY, B_P_FULL, B_FOLD_DONE, B_XCHG0, B_XCHG1
+  B_L_EMPTY, B_P_FULL, B_FOLD_DONE, B_XCHG0, B_XCHG1, B_W_FULL
 };
 
 // tensor-memory columns: Zr double buffer, L, S'
@@ -231,9 +231,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
 
   // ---------------- setup
   {
-    const uint4 *src = reinterpret_cast<const uint4 *>(p.wimg + (size_t)rank * kWImgBytes);
-    uint4 *dst = reinterpret_cast<uint4 *>(smem + kS2W);
-    for (int i = tid; i < kWImgBytes / 16; i += kThreads2) dst[i] = __ldg(src + i);
     for (int i = tid; i < kG; i += kThreads2) s_bias[i] = p.bias[rank * kG + i];
     if (tid < kDP) { s_sc[tid] = p.xscale[tid]; s_ncs[tid] = -(p.xshift[tid] * p.xscale[tid]); }
   }
@@ -246,7 +243,13 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     mbar_init(&bars[B_L_EMPTY], kWarpsWork); mbar_init(&bars[B_P_FULL], kWarpsWork);
     mbar_init(&bars[B_FOLD_DONE], kWarpsWork);
     mbar_init(&bars[B_XCHG0], 1); mbar_init(&bars[B_XCHG1], 1);
+    mbar_init(&bars[B_W_FULL], 1);
     fence_mbar_init();
+    // W' image of this rank: 64 KB bulk copy (async proxy), waited on by the MMA thread only
+    mbar_arrive_expect_tx(&bars[B_W_FULL], kWImgBytes);
+    for (int c = 0; c < 4; ++c)
+      bulk_g2s(sW + c * (kWImgBytes / 4), p.wimg + (size_t)rank * kWImgBytes + c * (kWImgBytes / 4), kWImgBytes / 4,
+               &bars[B_W_FULL]);
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -298,6 +301,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       const uint32_t idesc1 = idesc_f16_f32(128, kG, 0, 0);   // A = Zr (TMEM, K-major), B = W' K-major
       const uint32_t idesc2 = idesc_f16_f32(kNF, kG, 1, 1);   // A = Z^T (SMEM, MN-major), B = P MN-major
       uint32_t folds = 0;
+      mbar_wait(&bars[B_W_FULL], 0);
       auto gemm1 = [&](int i) {
         mbar_wait(&bars[B_ZR_FULL], i & 1);
         if (i >= 1) mbar_wait(&bars[B_L_EMPTY], (i - 1) & 1);

@@ -48,7 +48,7 @@ static_assert(kSmemWBytes <= 232448, "shared memory budget (wide)");
 
 enum : int {
   W_XFULL0 = 0, W_XFULL1, W_XEMPTY0, W_XEMPTY1, W_ZR_FULL, W_G1_DONE, W_G2A_DONE, W_G2_DONE,
-  W_L_EMPTY, W_P_FULL, W_ZB_FULL, W_FOLD_DONE, W_XCHG0, W_XCHG1
+  W_L_EMPTY, W_P_FULL, W_ZB_FULL, W_FOLD_DONE, W_XCHG0, W_XCHG1, W_W_FULL
 };
 
 // tensor-memory columns: Zr (half hf at 128 hf), L (64), S'_hf (64 each)
@@ -77,9 +77,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
 
   // ---------------- setup
   {
-    const uint4 *src = reinterpret_cast<const uint4 *>(p.wimg + (size_t)rank * kWImgBytes);
-    uint4 *dst = reinterpret_cast<uint4 *>(smem + kWW);
-    for (int i = tid; i < kWImgBytes / 16; i += kThreads2) dst[i] = __ldg(src + i);
     for (int i = tid; i < kGW; i += kThreads2) s_bias[i] = p.bias[rank * kGW + i];
     if (tid < kDMax) { s_sc[tid] = p.xscale[tid]; s_ncs[tid] = -(p.xshift[tid] * p.xscale[tid]); }
   }
@@ -92,7 +89,13 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
     mbar_init(&bars[W_L_EMPTY], kWarpsWork); mbar_init(&bars[W_P_FULL], kWarpsWork);
     mbar_init(&bars[W_ZB_FULL], kWarpsWork); mbar_init(&bars[W_FOLD_DONE], kWarpsWork);
     mbar_init(&bars[W_XCHG0], 1); mbar_init(&bars[W_XCHG1], 1);
+    mbar_init(&bars[W_W_FULL], 1);
     fence_mbar_init();
+    // W' image of this rank: 64 KB bulk copy (async proxy), waited on by the MMA thread only
+    mbar_arrive_expect_tx(&bars[W_W_FULL], kWImgBytes);
+    for (int c = 0; c < 4; ++c)
+      bulk_g2s(sW + c * (kWImgBytes / 4), p.wimg + (size_t)rank * kWImgBytes + c * (kWImgBytes / 4), kWImgBytes / 4,
+               &bars[W_W_FULL]);
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -145,6 +148,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       const uint32_t idesc1 = idesc_f16_f32(128, kGW, 0, 0);  // A = Zr (TMEM, K-major), B = W' K-major
       const uint32_t idesc2 = idesc_f16_f32(kNF, kGW, 1, 1);  // A = Z_hf^T (SMEM, MN-major), B = P MN-major
       uint32_t folds = 0;
+      mbar_wait(&bars[W_W_FULL], 0);
       auto gemm1 = [&](int i) {
         mbar_wait(&bars[W_ZR_FULL], i & 1);
         if (i >= 1) mbar_wait(&bars[W_L_EMPTY], (i - 1) & 1);
