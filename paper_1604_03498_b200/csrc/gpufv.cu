@@ -125,7 +125,7 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.off1 = o;     o = align_up(o + 16, 256);
   L.cstart = o;   o = align_up(o + (size_t)(L.ncl + 1) * 4, 256);
   L.cown = o;     o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 8, 256);
-  L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 12, 1024);  // double norm2[] + uint counters[]
+  L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * (kFinMaxParts * 8 + 4), 1024);  // norm parts + tickets
   L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * 4 * L.Kp * 4, 1024);
   L.slots = o;    o = align_up(o + (size_t)L.nslots * 2 * L.dpad * L.Kp * 4, 1024);
   L.hx = L.hoff = L.hout = 0;
@@ -279,7 +279,7 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.out = nullptr;
   f.stats_out = nullptr;
   f.norm2 = (double *)at(ws, L.norm2);
-  f.counters = (unsigned *)(f.norm2 + (batch > 0 ? batch : 1));
+  f.counters = (unsigned *)(f.norm2 + (size_t)(batch > 0 ? batch : 1) * kFinMaxParts);
   f.b_base = 0;
   f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
   f.mode = (int)(flags & FV_NORM_MASK);
@@ -290,7 +290,7 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
 fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStream_t st) {
 
   if (batch == 0) return FV_OK;
-  if (cudaMemsetAsync(f.norm2, 0, (size_t)batch * 12, st) != cudaSuccess) return cuda_check("memset norm2");
+  if (cudaMemsetAsync(f.counters, 0, (size_t)batch * 4, st) != cudaSuccess) return cuda_check("memset tickets");
   for (int b0 = 0; b0 < batch; b0 += 65535) {  // gridDim.y limit
     FinParams fc = f;
     fc.b_base = b0;

@@ -199,7 +199,7 @@ struct FinParams {
   const float *xscale;
   float *out;                 // batch x 2KD
   double *stats_out;          // k_reduce_stats output
-  double *norm2;              // batch (zeroed before k_finalize)
+  double *norm2;              // batch x kFinMaxParts: each block's partial sum of squares (fixed slots)
   unsigned *counters;         // batch (zeroed before k_finalize): last-block ticket
   int batch, K, Kp, D, ncl, mode;
   int dpad;                   // 64 (k_stats) or 128 (k_stats_w): slot rows = [lin 0..dpad-1 | quad 0..dpad-1]
@@ -207,6 +207,7 @@ struct FinParams {
 };
 
 constexpr int kFinJ = 32;       // Gaussians per finalize block
+constexpr int kFinMaxParts = (kMaxK / kFinJ) * (kDMax / kDP);  // finalize blocks per image
 constexpr int kFinKI = kDP / 8; // dims per thread: k = kq + 8 i
 
 // S0_j (gamma units) and S1_jk, S2_jk (about c, unscaled; k = kq + 8 i) of image b from the slots:
@@ -415,15 +416,16 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   if (tid == 0) {
     double tot = 0.0;
     for (int w = 0; w < 8; ++w) tot += s_red[w];
-    if (tot != 0.0) atomicAdd(p.norm2 + b, tot);
+    p.norm2[(size_t)b * kFinMaxParts + blockIdx.z * gridDim.x + blockIdx.x] = tot;  // own slot: no atomics
     __threadfence();
-    const unsigned ticket = atomicAdd(p.counters + b, 1u);
+    const unsigned ticket = atomicAdd(p.counters + b, 1u);  // only decides which block is last
     s_last = (ticket == gridDim.x * gridDim.z - 1);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const double n2 = *((volatile double *)(p.norm2 + b));
+  double n2 = 0.0;  // fixed-order sum of the parts: bitwise repeatable
+  for (unsigned k = 0; k < gridDim.x * gridDim.z; ++k) n2 += __ldcg(p.norm2 + (size_t)b * kFinMaxParts + k);
   if (!(n2 > 0.0)) return;
   const float sc = (float)(1.0 / sqrt(n2));
   float4 *ob = reinterpret_cast<float4 *>(p.out + (size_t)b * 2 * KD);  // 2KD % 4 == 0 (D % 4 == 0)

@@ -41,7 +41,6 @@ constexpr int kWarpsWork = 16;
 constexpr int kWarpMma = kWarpsWork, kWarpTma = kWarpsWork + 1;
 constexpr int kThreads2 = (kWarpTma + 1) * 32;  // 576
 constexpr int kMaxC2 = 2;                        // K <= 256 in this kernel (larger K: k_stats_w)
-constexpr int kMaxK = 512;                       // both tile families
 
 // per-tile metadata published by the TMA thread (ring of 4: slot t % 4 stays valid well past tile t)
 struct TileMeta {

@@ -187,12 +187,17 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         const bool chunk_first = (tw.meta().flags & 2) != 0;
         mbar_wait(&bars[W_P_FULL], i & 1);  // P(i) and Z_a(i) in shared memory
         if (chunk_first && i > 0) { mbar_wait(&bars[W_FOLD_DONE], folds & 1); ++folds; }
+        TR(10);
         gemm2(0, chunk_first);
         mma_commit(&bars[W_G2A_DONE]);
+        TR(11);
         mbar_wait(&bars[W_ZB_FULL], i & 1);  // Z_b(i)
+        TR(12);
         gemm2(1, chunk_first);
         mma_commit(&bars[W_G2_DONE]);
+        TR(13);
         if (i + 1 < n) gemm1(i + 1);
+        TR(14);
       }
     }
   } else {
@@ -279,7 +284,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
     bool prev_fold = false, chunk_seg_first = true;
     if (n > 0) { conv_half(0, 0); conv_half(0, 1); }
     for (int i = 0; i < n; ++i) {
+      TRW(0);
       work_wait(&bars[W_G1_DONE], i & 1);  // L(i) ready
+      TRW(1);
       // ---- softmax(i), online form (see k_stats): quarter h = 16 Gaussian columns
       float v[16];
       {
@@ -316,7 +323,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       }
       float2 *red = s_red + (i & 1) * (4 * kTileM);
       red[h * kTileM + row] = make_float2(m, sacc.x + sacc.y);
+      TRW(2);
       named_bar_sync(kBarLane0 + q, 128);
+      TRW(3);
       float M, S;
       {
         const float2 r0 = red[row], r1 = red[kTileM + row], r2 = red[2 * kTileM + row], r3 = red[3 * kTileM + row];
@@ -334,7 +343,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
           for (uint32_t r2 = 0; r2 < C; ++r2)
             if (r2 != rank) st_async_v2f32(mapa_shared(my, r2), M, S, mapa_shared(mybar, r2));
         }
+        TRW(12);
         mbar_wait(&bars[W_XCHG0 + par], (i >> 1) & 1);
+        TRW(13);
         float Mg = M;
         for (uint32_t r2 = 0; r2 < C; ++r2)
           if (r2 != rank) Mg = fmaxf(Mg, xb[r2 * kTileM + row].x);
@@ -346,6 +357,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       }
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
       if (row >= mt.nrows) alpha_p = 0.f;
+      TRW(4);
 
       // ---- GEMM2(i-1) (both halves) done: S' chunk complete (fold), Z and P free
       if (i >= 1) {
@@ -358,6 +370,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         }
       }
       if (mt.flags & 2) chunk_seg_first = (mt.flags & 8) != 0;
+      TRW(5);
 
       // ---- P(i) = gamma 2^14 (thresholded) -> fp16 hi/lo (one 128 B row of 64 Gaussians), S0
       const float2 ap = make_float2(alpha_p, alpha_p);
@@ -383,19 +396,25 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
 #pragma unroll
         for (int j = 0; j < 16; ++j) { int gj = rank * kGW + 16 * h + j; if (gj < p.K) go[gj] = v[j] * (1.f / kPScale); }
       }
+      TRW(6);
       copy_z(0);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[W_P_FULL]);
+      TRW(7);
       if (i + 1 < n) conv_half(i + 1, 0);  // Zr half a of tile i is consumed (GEMM1(i), copy_z(0))
+      TRW(8);
       work_wait(&bars[W_G2A_DONE], i & 1);  // GEMM2a(i) done reading Z
+      TRW(9);
       copy_z(1);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[W_ZB_FULL]);
+      TRW(10);
       if (i + 1 < n) conv_half(i + 1, 1);
+      TRW(11);
       if (mt.flags & 1) {  // segment end: S0 (units of 2^14 gamma), this warp's 32 rows -> partial slot q
         float t32[32];
 #pragma unroll
