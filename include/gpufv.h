@@ -87,8 +87,12 @@ fv_status fv_encode_batched(const float *X, const int64_t *offsets, int batch, i
                             fv_stream_t stream);
 
 /* Same as fv_encode_batched but X_host / offsets_host / out_host are HOST buffers (pinned for full
- * PCIe speed); the GMM arrays stay device pointers (a resident model).  Copies in, encodes, copies out
- * on `stream` and synchronises it before returning.  ws >= fv_workspace_bytes_host(...). */
+ * PCIe speed); the GMM arrays stay device pointers (a resident model).  The batch is processed in up to
+ * 16 image chunks: the host->device copy of chunk k+1 and the device->host copy of chunk k-1 run on two
+ * internal streams (created and destroyed by the call) while chunk k is encoded on `stream`; the call
+ * synchronises all three before returning.  Each chunk runs the device path on its own images, so
+ * results equal fv_encode_batched's to rounding (same images, different static schedule) and are
+ * bitwise repeatable across calls.  ws >= fv_workspace_bytes_host(...). */
 fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total,
                                  int D, const float *weights, const float *means, const float *sigmas, int K,
                                  float threshold, unsigned flags, float *out_host, void *ws, size_t ws_bytes,

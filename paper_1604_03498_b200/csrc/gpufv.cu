@@ -396,16 +396,55 @@ fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_hos
   float *dX = (float *)at(ws, L.hx);
   int64_t *doff = (int64_t *)at(ws, L.hoff);
   float *dout = (float *)at(ws, L.hout);
-  if (n_total > 0 && cudaMemcpyAsync(dX, X_host, (size_t)n_total * D * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return cuda_check("H2D X");
   if (cudaMemcpyAsync(doff, offsets_host, (size_t)(batch + 1) * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return cuda_check("H2D offsets");
-  if (fv_status s = encode_batched_impl(dX, doff, batch, n_total, D, w, mu, sg, K, thr, flags, dout, ws, ws_bytes, st, &L))
-    return s;
-  if (batch > 0 && cudaMemcpyAsync(out_host, dout, (size_t)batch * 2 * K * D * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-    return cuda_check("D2H out");
-  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("stream sync");
-  return FV_OK;
+  if (!(flags & FV_PREPARED))
+    if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
+  if (batch == 0) return cudaStreamSynchronize(st) == cudaSuccess ? FV_OK : cuda_check("stream sync");
+  // Pipelined in image chunks: the H2D copy of chunk k+1 (stream `cin`) and the D2H copy of chunk k-1
+  // (stream `cout`) overlap the encode of chunk k on `stream`; events order each chunk's three steps.
+  const size_t fv_floats = (size_t)2 * K * D;
+  const int nch = std::max(1, std::min(batch, 16));
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t ev[2 * 16] = {};
+  fv_status rs = FV_OK;
+  auto cleanup = [&]() {
+    for (auto &e : ev) if (e) cudaEventDestroy(e);
+    if (cin) cudaStreamDestroy(cin);
+    if (cout) cudaStreamDestroy(cout);
+  };
+  if (cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking) != cudaSuccess) {
+    rs = cuda_check("stream create");
+    cleanup();
+    return rs;
+  }
+  for (int k = 0; k < 2 * nch && rs == FV_OK; ++k)
+    if (cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming) != cudaSuccess) rs = cuda_check("event create");
+  for (int k = 0; k < nch && rs == FV_OK; ++k) {
+    const int b0 = (int)((int64_t)k * batch / nch), b1 = (int)((int64_t)(k + 1) * batch / nch);
+    const int64_t r0 = offsets_host[b0], r1 = offsets_host[b1];
+    if (r1 > r0 && cudaMemcpyAsync(dX + r0 * D, X_host + r0 * D, (size_t)(r1 - r0) * D * 4, cudaMemcpyHostToDevice,
+                                   cin) != cudaSuccess) { rs = cuda_check("H2D X"); break; }
+    cudaEventRecord(ev[2 * k], cin);
+    cudaStreamWaitEvent(st, ev[2 * k], 0);
+    // the chunk's images through the device path: absolute row offsets into the staged X
+    rs = encode_batched_impl(dX, doff + b0, b1 - b0, n_total, D, w, mu, sg, K, thr, flags | FV_PREPARED,
+                             dout + (size_t)b0 * fv_floats, ws, ws_bytes, st, &L);
+    if (rs != FV_OK) break;
+    cudaEventRecord(ev[2 * k + 1], st);
+    cudaStreamWaitEvent(cout, ev[2 * k + 1], 0);
+    if (cudaMemcpyAsync(out_host + (size_t)b0 * fv_floats, dout + (size_t)b0 * fv_floats,
+                        (size_t)(b1 - b0) * fv_floats * 4, cudaMemcpyDeviceToHost, cout) != cudaSuccess) {
+      rs = cuda_check("D2H out");
+      break;
+    }
+  }
+  if (cudaStreamSynchronize(cout) != cudaSuccess || cudaStreamSynchronize(cin) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    if (rs == FV_OK) rs = cuda_check("stream sync");
+  cleanup();
+  return rs;
 }
 
 fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D, const float *w,
