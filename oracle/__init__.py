@@ -20,6 +20,7 @@ from .oracle import (  # noqa: F401
     max_threads,
     normalize,
     posteriors,
+    score,
     stats,
     stats_batched,
 )

@@ -184,3 +184,18 @@ def fv_from_stats(st, priors, means, variances, mode: int = NORM_IMPROVED) -> np
     U = (S1 - mp * S0[:, None]) / np.sqrt(v)
     V = (S2 - 2 * mp * S1 + mp * mp * S0[:, None]) / v - S0[:, None]
     return normalize(np.concatenate([U.ravel(), V.ravel()]), w, N, mode)
+
+
+def score(fv, W, bias=None) -> np.ndarray:
+    """Linear decision values of a linear classifier on Fisher vectors (the
+    paper trains "a classification model with liblinear" on the frame FVs and predicts per frame,
+    P:563-564):  s_bc = sum_d W_cd fv_bd + b_c, in double precision (one matmul).
+    fv: (batch, 2KD) or (2KD,); W: (n_cls, 2KD); bias: (n_cls,) or None (zero)."""
+    fv = _d(fv)
+    W = _d(W)
+    if W.ndim == 1:
+        W = W[None]
+    s = np.atleast_2d(fv) @ W.T
+    if bias is not None:
+        s = s + _d(bias)[None, :]
+    return s if fv.ndim == 2 else s[0]

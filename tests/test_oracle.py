@@ -314,3 +314,36 @@ def test_generator_is_deterministic_and_shaped():
     assert gmm[0].dtype == np.float32 and gmm[1].shape == (256, 64) and np.all(gmm[2] > 0)
     a = fvgen.make_descriptors(gmm, 1000, 7); b = fvgen.make_descriptors(gmm, 1000, 7)
     assert np.array_equal(a, b) and a.shape == (1000, 64)
+
+
+# ---------------------------------------------------------------- linear scoring (NEXT-4)
+def test_score_closed_form_descriptor_at_mean():
+    """K=1, one descriptor at mu: FV = [0..0, -1/sqrt(D)..] (A9), so the all-ones classifier scores
+    -sqrt(D) + b and a U-only classifier scores b (closed forms; P:563-564 linear model)."""
+    D = 6
+    mu = np.random.default_rng(5).normal(size=(1, D))
+    fv = oracle.encode(mu, [0.5], mu, np.ones((1, D)) * 0.3)
+    W = np.stack([np.ones(2 * D), np.r_[np.ones(D), np.zeros(D)]])
+    s = oracle.score(fv, W, [0.25, -1.5])
+    np.testing.assert_allclose(s, [-np.sqrt(D) + 0.25, -1.5], rtol=1e-13, atol=1e-13)
+
+
+def test_score_self_similarity_basis_and_linearity():
+    """W = the (unit-norm) FVs themselves gives 1 on the diagonal (A9 unit norm); basis rows pick
+    components; the score is linear in W and shifts by b (the plain definition, checked on a batch so
+    a transposed W or a dropped bias fails)."""
+    gmm = fvgen.make_gmm(8, 4, seed=31)
+    X, off = fvgen.make_batch(gmm, [120, 80, 200], seed_base=32)
+    F = oracle.encode_batched(X, off, *gmm)
+    S = oracle.score(F, F)
+    np.testing.assert_allclose(np.diag(S), 1.0, rtol=1e-12)
+    assert np.all(np.abs(S - S.T) < 1e-12) and np.all(S <= 1 + 1e-12)
+    idx = [0, 5, 2 * 8 * 4 - 1]
+    E = np.eye(F.shape[1])[idx]
+    np.testing.assert_array_equal(oracle.score(F, E, np.zeros(3)), F[:, idx])
+    rng = np.random.default_rng(33)
+    W1, W2 = rng.normal(size=(2, F.shape[1])), rng.normal(size=(2, F.shape[1]))
+    b = np.array([0.5, -2.0])
+    np.testing.assert_allclose(oracle.score(F, 2 * W1 - W2, b), 2 * oracle.score(F, W1) - oracle.score(F, W2) + b,
+                               rtol=1e-12, atol=1e-12)
+    assert oracle.score(F[1], W1).shape == (2,)
