@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--score-steps", type=int, default=5,
+                    help="steps of the fused-scoring monitoring leg (NEXT-4; 0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="wall budget of the oracle sample")
     ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
                     help="c4: frame-sharded stream (default, the metric's config); c5: one 10M x 128 set, K=512, "
@@ -230,6 +232,16 @@ def load_peaks():
         return {}
 
 
+def tensor_peak():
+    """(TFLOP/s, source) for a kernel timed inside a long step: MEASURED_PEAKS.json's sustained cuBLAS
+    bf16 figure (kind::f16 runs at the bf16 rate), else the profiling guide's stated fallback."""
+    pk = load_peaks()
+    if "bf16_tflops_sustained" in pk:
+        return float(pk["bf16_tflops_sustained"]), "of measured: MEASURED_PEAKS.json bf16_tflops_sustained (kind::f16 = bf16 rate)"
+    return 1400.0, ("of fallback: MEASURED_PEAKS.json absent; B200_PROFILING.md fallback 1.59 PF burst, "
+                    "~1.4 PF sustained under the power cap (kind::f16 = bf16 rate)")
+
+
 def run_c5(args, rank, world, local):
     """C5 (BASELINE.json configs[4]): one set of args.c5_n descriptors, D=128, K=512, exact posteriors,
     descriptor-sharded over the ranks: each rank computes the fp64 sufficient
@@ -348,7 +360,7 @@ def run_c5(args, rank, world, local):
             torch.distributed.destroy_process_group()
         return
     flop = 4 * K5 * (2 * D5 + 1)
-    peak_tf = load_peaks().get("bf16_tflops_sustained", 1400.0)
+    peak_tf, peak_src = tensor_peak()
     achieved = flop * n / (kms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -363,7 +375,7 @@ def run_c5(args, rank, world, local):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf, "traffic": None, "kernel": "k_stats_w", "kernel_ms": kms,
                      "kernel_share_of_step": kms / (total_ms / args.steps), "flop_per_desc": flop,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kind::f16 = bf16 rate)"},
+                     "peak_source": peak_src},
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches[0] * args.steps, "parity": parity,
         "cpu_baseline": None,
     }
@@ -484,6 +496,63 @@ def main():
                "note": "fv_encode_batched_host: pinned host X -> device, encode, FVs -> pinned host, pipelined in 16 image chunks over 3 streams; host clock"}
         del Xh, outh, wsh
 
+    # monitoring leg (NEXT-4): the same stream scored by a linear classifier fused into the finalize,
+    # FVs never written; device-timed and end to end through the host entry point (scores only back)
+    monitoring = None
+    if args.score_steps > 0:
+        n_cls = 1
+        rng = np.random.default_rng(1604 + 7)
+        Wd = torch.from_numpy(rng.standard_normal((n_cls, 2 * K * D)).astype(np.float32)).to(dev)
+        bd = torch.zeros(n_cls, dtype=torch.float32, device=dev)
+        wss = fv.Workspace(device=dev)
+        wss.ensure(int(fv.lib.fv_workspace_bytes_scored(n_total, frames, K, D, n_cls, 0, 0)))
+        fv.gmm_prepare(gmm, wss)
+        for _ in range(3):
+            fv.encode_scored_batched(Xd, offd, gmm, Wd, bd, threshold=TAU, ws=wss, prepared=True)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record(stream)
+        for _ in range(args.score_steps):
+            fv.encode_scored_batched(Xd, offd, gmm, Wd, bd, threshold=TAU, ws=wss, prepared=True)
+        b_ev.record(stream)
+        torch.cuda.synchronize(dev)
+        sms = a_ev.elapsed_time(b_ev) / args.score_steps
+        if world > 1:
+            t = torch.tensor([sms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            sms = float(t.item())
+        monitoring = {"n_cls": n_cls, "value": world * n_total / (sms * 1e-3), "unit": UNIT, "ms_per_step": sms,
+                      "frames_per_s": world * frames / (sms * 1e-3), "steps": args.score_steps,
+                      "note": "fv_encode_scored_batched (FV . w + b fused into k_finalize, FVs not written), "
+                              "same C4 stream; device-timed, max over ranks"}
+        del wss
+        if args.e2e_steps > 0:
+            Xh = torch.from_numpy(X).pin_memory()
+            offh = torch.from_numpy(offsets)
+            sh = torch.empty(frames, n_cls, dtype=torch.float32).pin_memory()
+            wsh = fv.Workspace(device=dev)
+            wsh.ensure(int(fv.lib.fv_workspace_bytes_scored(n_total, frames, K, D, n_cls, 1, 0)))
+            fv.gmm_prepare(gmm, wsh)
+            fv.encode_scored_batched_host(Xh, offh, gmm, Wd, bd, threshold=TAU, ws=wsh, prepared=True, scores_host=sh)
+            if world > 1:
+                torch.distributed.barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                fv.encode_scored_batched_host(Xh, offh, gmm, Wd, bd, threshold=TAU, ws=wsh, prepared=True,
+                                              scores_host=sh)
+            el = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([el], dtype=torch.float64, device=dev)
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                el = float(t.item())
+            monitoring["e2e"] = {"value": world * n_total * args.e2e_steps / el, "unit": UNIT,
+                                 "h2d_bytes_per_step": int(Xh.numel() * 4 + offh.numel() * 8),
+                                 "d2h_bytes_per_step": int(sh.numel() * 4),
+                                 "note": "fv_encode_scored_batched_host: pinned host X in, scores out; host clock"}
+            del Xh, sh, wsh
+
     # single-frame latency (C2 shape: one 5000-descriptor frame), eager and CUDA-graph captured
     latency = None
     if not args.no_latency:
@@ -530,7 +599,7 @@ def main():
             torch.distributed.destroy_process_group()
         return
 
-    peak_tf = load_peaks().get("bf16_tflops_sustained", 1400.0)  # kind::f16 (fp16) runs at the bf16 rate
+    peak_tf, peak_src = tensor_peak()
     kms = statistics.mean(kstats_ms)
     achieved = FLOP_PER_DESC * n_total / (kms * 1e-3) / 1e12
     traffic = None
@@ -557,12 +626,13 @@ def main():
                      "kernel": "k_stats", "kernel_ms": kms, "kernel_share_of_step": kms / ms_per_step,
                      "flop_per_desc": FLOP_PER_DESC,
                      "issued_tensor_frac": achieved * ISSUED_FLOP_PER_DESC / FLOP_PER_DESC / peak_tf,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kind::f16 = bf16 rate)"},
+                     "peak_source": peak_src},
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "parity": parity,
         "frame_latency": latency,
+        "monitoring": monitoring,
         "cpu_baseline": cpu,
         "context": {"paper": "34 ms per 320x240 frame and ~12x over 1-thread CPU, end-to-end incl. dense SIFT, "
                              "Tesla K40 (PAPER.md:577-578, :452-455); not comparable, context only"},

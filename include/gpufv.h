@@ -98,6 +98,31 @@ fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_hos
                                  float threshold, unsigned flags, float *out_host, void *ws, size_t ws_bytes,
                                  fv_stream_t stream);
 
+/* Fused linear scoring (the paper's video-monitoring application trains "a
+ * classification model with liblinear" on per-frame FVs and predicts every frame):
+ *   scores[b * n_cls + c] = sum_d svm_w[c * 2KD + d] * fv_b[d] + svm_b[c]
+ * where fv_b is image b's FV exactly as fv_encode_batched would return it (same flags/normalisation).
+ * svm_w: device, n_cls x 2KD fp32 (row c laid out like one FV: U block then V block); svm_b: device,
+ * n_cls fp32 or NULL (zero bias); 1 <= n_cls <= 32 (else FV_ERR_ARG).  The dot products are taken in
+ * the finalize kernel on the tile it has just computed (per-block partials in fixed slots, summed in
+ * block order, scaled by the image's 1/||z||): bitwise repeatable.  `out` (batch x 2KD) may be NULL:
+ * then the FVs never reach HBM and only batch x n_cls floats leave the kernel.
+ * ws >= fv_workspace_bytes_scored(n_total, batch, K, D, n_cls, 0, flags). */
+size_t fv_workspace_bytes_scored(int64_t n_total, int batch, int K, int D, int n_cls, int host_io, unsigned flags);
+fv_status fv_encode_scored_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D,
+                                   const float *weights, const float *means, const float *sigmas, int K,
+                                   float threshold, unsigned flags, const float *svm_w, const float *svm_b, int n_cls,
+                                   float *scores, float *out, void *ws, size_t ws_bytes, fv_stream_t stream);
+
+/* Host-buffer variant for the monitoring stream: X_host / offsets_host in (pinned host), scores_host
+ * (batch x n_cls) out; GMM and classifier stay device-resident.  Same chunked H2D / encode / D2H
+ * pipeline as fv_encode_batched_host, but only the scores cross PCIe back.
+ * ws >= fv_workspace_bytes_scored(n_total, batch, K, D, n_cls, 1, flags). */
+fv_status fv_encode_scored_batched_host(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total,
+                                        int D, const float *weights, const float *means, const float *sigmas, int K,
+                                        float threshold, unsigned flags, const float *svm_w, const float *svm_b,
+                                        int n_cls, float *scores_host, void *ws, size_t ws_bytes, fv_stream_t stream);
+
 /* Split path for descriptor sharding (a2-a6 without a7).  stats: batch x (1 + K(2D+1)) doubles,
  *   stats[b] = [ N_b, S0 (K), S1 (K x D), S2 (K x D) ],
  *   S0_j = sum_i gamma_ij,  S1_jk = sum_i gamma_ij (x_ik - c_k),  S2_jk = sum_i gamma_ij (x_ik - c_k)^2,

@@ -16,7 +16,7 @@ __all__ = [
     "NORM_IMPROVED", "NORM_POWER_L2", "NORM_NONE", "SIGMA_IS_STDDEV", "PREPARED",
     "GMM", "Workspace", "lib", "lib_path", "workspace_bytes", "gmm_prepare", "encode", "encode_batched",
     "encode_batched_host", "stats_batched", "finalize", "posteriors", "last_launch_count", "profile_events",
-    "FVError",
+    "encode_scored_batched", "encode_scored_batched_host", "MAX_CLASSES", "FVError",
 ]
 
 NORM_IMPROVED = 0
@@ -25,7 +25,8 @@ NORM_NONE = 2
 SIGMA_IS_STDDEV = 1 << 4
 DETERMINISTIC = 1 << 5
 PREPARED = 1 << 6
-_RAW_LOGLIK = 1 << 8  # test hook of fv_posteriors: raw log2-likelihoods instead of gamma
+_RAW_LOGLIK = 1 << 8
+MAX_CLASSES = 32  # test hook of fv_posteriors: raw log2-likelihoods instead of gamma
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libgpufv.so")
@@ -51,8 +52,14 @@ lib.fv_encode_batched_host.argtypes = lib.fv_encode_batched.argtypes
 lib.fv_stats_batched.argtypes = [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _i32, _f32, _u32, _vp, _vp, _sz, _vp]
 lib.fv_finalize.argtypes = [_vp, _i32, _i32, _vp, _vp, _vp, _i32, _u32, _vp, _vp, _sz, _vp]
 lib.fv_posteriors.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _f32, _u32, _vp, _vp, _sz, _vp]
+lib.fv_workspace_bytes_scored.argtypes = [_i64, _i32, _i32, _i32, _i32, _i32, _u32]
+lib.fv_workspace_bytes_scored.restype = _sz
+lib.fv_encode_scored_batched.argtypes = [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _i32, _f32, _u32, _vp, _vp, _i32,
+                                         _vp, _vp, _vp, _sz, _vp]
+lib.fv_encode_scored_batched_host.argtypes = [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _i32, _f32, _u32, _vp, _vp,
+                                              _i32, _vp, _vp, _sz, _vp]
 for _fn in ("fv_gmm_prepare", "fv_encode", "fv_encode_batched", "fv_encode_batched_host", "fv_stats_batched",
-            "fv_finalize", "fv_posteriors"):
+            "fv_finalize", "fv_posteriors", "fv_encode_scored_batched", "fv_encode_scored_batched_host"):
     getattr(lib, _fn).restype = _i32
 lib.fv_status_string.argtypes = [_i32]
 lib.fv_status_string.restype = _c.c_char_p
@@ -261,3 +268,60 @@ def posteriors(X, gmm: GMM, threshold: float = 0.0, raw_loglik: bool = False, ws
     _check(lib.fv_posteriors(_ptr(X), X.shape[0], gmm.D, w, m, s, gmm.K, float(threshold), flags, _ptr(g),
                              *ws.args(), _stream()))
     return g
+
+
+def _classifier(svm_w, svm_b, gmm: GMM):
+    dim = 2 * gmm.K * gmm.D
+    if not (svm_w.is_cuda and svm_w.dtype == torch.float32 and svm_w.is_contiguous()):
+        raise ValueError("svm_w must be a contiguous float32 CUDA tensor (n_cls, 2KD)")
+    W = svm_w.reshape(-1, dim)
+    if svm_b is not None and not (svm_b.is_cuda and svm_b.dtype == torch.float32 and svm_b.numel() == W.shape[0]):
+        raise ValueError("svm_b must be a float32 CUDA tensor (n_cls,)")
+    return W, W.shape[0]
+
+
+def encode_scored_batched(X, offsets, gmm: GMM, svm_w, svm_b=None, threshold: float = 0.0,
+                          mode: int = NORM_IMPROVED, ws: Workspace | None = None, prepared: bool = False,
+                          out=None, return_fv: bool = False):
+    """Fused linear scoring (NEXT-4): scores (batch, n_cls) = FV . svm_w^T + svm_b, taken in
+    the finalize kernel.  With return_fv (or an ``out`` tensor) the FVs are also written and returned
+    as (scores, fv); otherwise they never reach HBM."""
+    _check_X(X, gmm.D)
+    W, n_cls = _classifier(svm_w, svm_b, gmm)
+    B = offsets.shape[0] - 1
+    need = int(lib.fv_workspace_bytes_scored(X.shape[0], B, gmm.K, gmm.D, n_cls, 0, 0))
+    if need == 0:
+        raise FVError(1)
+    ws, grown = _ws(ws, need, X.device)
+    prepared = prepared and not grown
+    scores = torch.empty(B, n_cls, dtype=torch.float32, device=X.device)
+    if out is None and return_fv:
+        out = torch.empty(B, 2 * gmm.K * gmm.D, dtype=torch.float32, device=X.device)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_encode_scored_batched(_ptr(X), _ptr(offsets), B, X.shape[0], gmm.D, w, m, s, gmm.K,
+                                        float(threshold), _mode_flags(gmm, mode, prepared), _ptr(W), _ptr(svm_b),
+                                        n_cls, _ptr(scores), _ptr(out), *ws.args(), _stream()))
+    return (scores, out) if out is not None else scores
+
+
+def encode_scored_batched_host(X_host, offsets_host, gmm: GMM, svm_w, svm_b=None, threshold: float = 0.0,
+                               mode: int = NORM_IMPROVED, ws: Workspace | None = None, prepared: bool = False,
+                               scores_host=None):
+    """Monitoring-stream entry point: pinned host descriptors in, host scores (batch, n_cls) out; the
+    GMM and the classifier stay on the GPU and only the scores cross PCIe back."""
+    assert X_host.device.type == "cpu" and X_host.dtype == torch.float32 and X_host.is_contiguous()
+    assert offsets_host.device.type == "cpu" and offsets_host.dtype == torch.int64
+    W, n_cls = _classifier(svm_w, svm_b, gmm)
+    B = offsets_host.shape[0] - 1
+    need = int(lib.fv_workspace_bytes_scored(X_host.shape[0], B, gmm.K, gmm.D, n_cls, 1, 0))
+    if need == 0:
+        raise FVError(1)
+    ws, grown = _ws(ws, need, gmm.means.device)
+    prepared = prepared and not grown
+    if scores_host is None:
+        scores_host = torch.empty(B, n_cls, dtype=torch.float32, pin_memory=True)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_encode_scored_batched_host(_ptr(X_host), _ptr(offsets_host), B, X_host.shape[0], gmm.D, w, m, s,
+                                             gmm.K, float(threshold), _mode_flags(gmm, mode, prepared), _ptr(W),
+                                             _ptr(svm_b), n_cls, _ptr(scores_host), *ws.args(), _stream()))
+    return scores_host

@@ -96,11 +96,12 @@ struct Layout {
   int64_t n_total, nslots;                                         // segment slots (cluster, image)
   size_t wimg, bias, xshift, xscale, cshift, bscratch, coef;  // prepared GMM (head of ws)
   size_t tiles, off1, cstart, cown, norm2, s0slots, slots;  // per call
+  size_t spart;                                           // fused scoring partial dots (n_cls > 0)
   size_t hx, hoff, hout;                                  // _host entry point
   size_t total;
 };
 
-bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout &L) {
+bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout &L, int n_cls = 0) {
   L.C = cluster_size(K, D);
   L.Kp = L.C * gauss_per_cta(K, D);
   L.dpad = is_wide(K, D) ? kDMax : kDP;
@@ -128,11 +129,13 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * (kFinMaxParts * 8 + 4), 1024);  // norm parts + tickets
   L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * 4 * L.Kp * 4, 1024);
   L.slots = o;    o = align_up(o + (size_t)L.nslots * 2 * L.dpad * L.Kp * 4, 1024);
+  L.spart = o;    o = align_up(o + (size_t)(n_cls > 0 ? batch : 0) * kFinMaxParts * n_cls * 8, 1024);
   L.hx = L.hoff = L.hout = 0;
   if (host_io) {
+    // device staging of X, offsets and the per-image result (scores when n_cls > 0, else FVs)
     L.hx = o;   o = align_up(o + (size_t)n_total * D * 4, 1024);
     L.hoff = o; o = align_up(o + (size_t)(batch + 1) * 8, 256);
-    L.hout = o; o = align_up(o + (size_t)batch * 2 * K * D * 4, 1024);
+    L.hout = o; o = align_up(o + (size_t)batch * (n_cls > 0 ? n_cls : 2 * K * D) * 4, 1024);
   }
   L.total = o;
   return true;
@@ -281,6 +284,8 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.norm2 = (double *)at(ws, L.norm2);
   f.counters = (unsigned *)(f.norm2 + (size_t)(batch > 0 ? batch : 1) * kFinMaxParts);
   f.b_base = 0;
+  f.svm_w = nullptr; f.svm_b = nullptr; f.scores = nullptr; f.n_cls = 0;
+  f.spart = (double *)at(ws, L.spart);
   f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
   f.mode = (int)(flags & FV_NORM_MASK);
   f.dpad = L.dpad;
@@ -300,12 +305,20 @@ fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStrea
   return cuda_check("k_finalize");
 }
 
+// Fused linear scoring arguments (NEXT-4); n_cls == 0: plain encode.
+struct Scoring {
+  const float *w = nullptr, *b = nullptr;
+  int n_cls = 0;
+  float *scores = nullptr;
+};
+
 fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D,
                               const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
-                              float *out, void *ws, size_t ws_bytes, cudaStream_t st, const Layout *Lin) {
+                              float *out, void *ws, size_t ws_bytes, cudaStream_t st, const Layout *Lin,
+                              const Scoring &sc = Scoring()) {
   Layout L;
   if (Lin) L = *Lin;
-  else if (!make_layout(n_total, batch, K, D, false, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  else if (!make_layout(n_total, batch, K, D, false, L, sc.n_cls)) return fail(FV_ERR_CUDA, "occupancy query failed");
   if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
   if (!(flags & FV_PREPARED))
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
@@ -313,7 +326,14 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st)) return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   f.out = out;
+  f.svm_w = sc.w; f.svm_b = sc.b; f.n_cls = sc.n_cls; f.scores = sc.scores;
   return launch_finalize(f, batch, K, D, st);
+}
+
+fv_status check_scoring(const float *svm_w, int n_cls, const float *scores, int batch) {
+  if (n_cls < 1 || n_cls > kMaxCls) return fail(FV_ERR_ARG, "n_cls=%d must be in [1, %d]", n_cls, kMaxCls);
+  if (!svm_w || (batch > 0 && !scores)) return fail(FV_ERR_ARG, "null classifier weights/scores");
+  return FV_OK;
 }
 
 fv_status check_common(const float *X, int64_t n_total, int batch, int D, int K, float thr, const float *w,
@@ -382,20 +402,21 @@ fv_status fv_encode(const float *X, int64_t N, int D, const float *w, const floa
   return encode_batched_impl(X, nullptr, 1, N, D, w, mu, sg, K, thr, flags, out, ws, ws_bytes, (cudaStream_t)stream, &L);
 }
 
-fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total, int D,
-                                 const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
-                                 float *out_host, void *ws, size_t ws_bytes, fv_stream_t stream) {
-  g_launches = 0;
-  if (fv_status s = check_common(X_host, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
-  if (batch > 0 && (!offsets_host || !out_host)) return fail(FV_ERR_ARG, "null offsets/out");
-  if (fv_status s = check_device()) return s;
+}  // extern "C"
+
+namespace {
+
+// Host-buffer pipeline shared by fv_encode_batched_host and fv_encode_scored_batched_host: the result
+// per image is the FV (2KD floats) or, with scoring, its n_cls scores.
+fv_status encode_host_impl(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total, int D,
+                           const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
+                           float *res_host, const Scoring &sc_in, void *ws, size_t ws_bytes, cudaStream_t st) {
   Layout L;
-  if (!make_layout(n_total, batch, K, D, true, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (!make_layout(n_total, batch, K, D, true, L, sc_in.n_cls)) return fail(FV_ERR_CUDA, "occupancy query failed");
   if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
-  cudaStream_t st = (cudaStream_t)stream;
   float *dX = (float *)at(ws, L.hx);
   int64_t *doff = (int64_t *)at(ws, L.hoff);
-  float *dout = (float *)at(ws, L.hout);
+  float *dres = (float *)at(ws, L.hout);
   if (cudaMemcpyAsync(doff, offsets_host, (size_t)(batch + 1) * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return cuda_check("H2D offsets");
   if (!(flags & FV_PREPARED))
@@ -403,7 +424,7 @@ fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_hos
   if (batch == 0) return cudaStreamSynchronize(st) == cudaSuccess ? FV_OK : cuda_check("stream sync");
   // Pipelined in image chunks: the H2D copy of chunk k+1 (stream `cin`) and the D2H copy of chunk k-1
   // (stream `cout`) overlap the encode of chunk k on `stream`; events order each chunk's three steps.
-  const size_t fv_floats = (size_t)2 * K * D;
+  const size_t per_image = sc_in.n_cls > 0 ? (size_t)sc_in.n_cls : (size_t)2 * K * D;
   const int nch = std::max(1, std::min(batch, 16));
   cudaStream_t cin = nullptr, cout = nullptr;
   cudaEvent_t ev[2 * 16] = {};
@@ -429,14 +450,17 @@ fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_hos
     cudaEventRecord(ev[2 * k], cin);
     cudaStreamWaitEvent(st, ev[2 * k], 0);
     // the chunk's images through the device path: absolute row offsets into the staged X
-    rs = encode_batched_impl(dX, doff + b0, b1 - b0, n_total, D, w, mu, sg, K, thr, flags | FV_PREPARED,
-                             dout + (size_t)b0 * fv_floats, ws, ws_bytes, st, &L);
+    Scoring sc = sc_in;
+    float *out = dres + (size_t)b0 * per_image;
+    if (sc.n_cls > 0) { sc.scores = out; out = nullptr; }
+    rs = encode_batched_impl(dX, doff + b0, b1 - b0, n_total, D, w, mu, sg, K, thr, flags | FV_PREPARED, out, ws,
+                             ws_bytes, st, &L, sc);
     if (rs != FV_OK) break;
     cudaEventRecord(ev[2 * k + 1], st);
     cudaStreamWaitEvent(cout, ev[2 * k + 1], 0);
-    if (cudaMemcpyAsync(out_host + (size_t)b0 * fv_floats, dout + (size_t)b0 * fv_floats,
-                        (size_t)(b1 - b0) * fv_floats * 4, cudaMemcpyDeviceToHost, cout) != cudaSuccess) {
-      rs = cuda_check("D2H out");
+    if (cudaMemcpyAsync(res_host + (size_t)b0 * per_image, dres + (size_t)b0 * per_image,
+                        (size_t)(b1 - b0) * per_image * 4, cudaMemcpyDeviceToHost, cout) != cudaSuccess) {
+      rs = cuda_check("D2H result");
       break;
     }
   }
@@ -445,6 +469,59 @@ fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_hos
     if (rs == FV_OK) rs = cuda_check("stream sync");
   cleanup();
   return rs;
+}
+
+}  // namespace
+
+extern "C" {
+
+fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total, int D,
+                                 const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
+                                 float *out_host, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_common(X_host, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
+  if (batch > 0 && (!offsets_host || !out_host)) return fail(FV_ERR_ARG, "null offsets/out");
+  if (fv_status s = check_device()) return s;
+  return encode_host_impl(X_host, offsets_host, batch, n_total, D, w, mu, sg, K, thr, flags, out_host, Scoring(), ws,
+                          ws_bytes, (cudaStream_t)stream);
+}
+
+size_t fv_workspace_bytes_scored(int64_t n_total, int batch, int K, int D, int n_cls, int host_io, unsigned flags) {
+  (void)flags;
+  Layout L;
+  if (K < 1 || K > kMaxK || batch < 0 || n_total < 0 || n_cls < 1 || n_cls > kMaxCls) return 0;
+  if (!make_layout(n_total, batch, K, D, host_io != 0, L, n_cls)) return 0;
+  return L.total;
+}
+
+fv_status fv_encode_scored_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D,
+                                   const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
+                                   const float *svm_w, const float *svm_b, int n_cls, float *scores, float *out,
+                                   void *ws, size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_common(X, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
+  if (batch > 0 && !offsets) return fail(FV_ERR_ARG, "null offsets");
+  if (fv_status s = check_scoring(svm_w, n_cls, scores, batch)) return s;
+  if (fv_status s = check_device()) return s;
+  Scoring sc;
+  sc.w = svm_w; sc.b = svm_b; sc.n_cls = n_cls; sc.scores = scores;
+  return encode_batched_impl(X, offsets, batch, n_total, D, w, mu, sg, K, thr, flags, out, ws, ws_bytes,
+                             (cudaStream_t)stream, nullptr, sc);
+}
+
+fv_status fv_encode_scored_batched_host(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total,
+                                        int D, const float *w, const float *mu, const float *sg, int K, float thr,
+                                        unsigned flags, const float *svm_w, const float *svm_b, int n_cls,
+                                        float *scores_host, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_common(X_host, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
+  if (batch > 0 && !offsets_host) return fail(FV_ERR_ARG, "null offsets");
+  if (fv_status s = check_scoring(svm_w, n_cls, scores_host, batch)) return s;
+  if (fv_status s = check_device()) return s;
+  Scoring sc;
+  sc.w = svm_w; sc.b = svm_b; sc.n_cls = n_cls;
+  return encode_host_impl(X_host, offsets_host, batch, n_total, D, w, mu, sg, K, thr, flags, scores_host, sc, ws,
+                          ws_bytes, (cudaStream_t)stream);
 }
 
 fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D, const float *w,

@@ -204,7 +204,15 @@ struct FinParams {
   int batch, K, Kp, D, ncl, mode;
   int dpad;                   // 64 (k_stats) or 128 (k_stats_w): slot rows = [lin 0..dpad-1 | quad 0..dpad-1]
   int b_base;                 // first image of this launch (gridDim.y <= 65535 images per launch)
+  // fused linear scoring (NEXT-4): scores[b][c] = svm_w[c] . fv_b + svm_b[c]; n_cls == 0: off
+  const float *svm_w;         // n_cls x 2KD (same layout as one FV)
+  const float *svm_b;         // n_cls (nullptr: zero bias)
+  float *scores;              // batch x n_cls
+  double *spart;              // batch x kFinMaxParts x n_cls: each block's partial dot products
+  int n_cls;
 };
+
+constexpr int kMaxCls = 32;     // classes of the fused linear scoring
 
 constexpr int kFinJ = 32;       // Gaussians per finalize block
 constexpr int kFinMaxParts = (kMaxK / kFinJ) * (kDMax / kDP);  // finalize blocks per image
@@ -256,10 +264,15 @@ __device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int 
 // the global stores are coalesced over (j, k).  The Eq. (6)-(7) combination runs in fp64; the signed
 // square root (reading A9) in fp32 on the rounded value.  The L2 norm is accumulated with one
 // atomic per block and the LAST block of each image (ticket) rescales it.
+// Fused linear scoring (NEXT-4): each block also writes the dot products of its (pre-L2)
+// U/V tile with the n_cls classifier rows into its own partial slot; the last block sums the slots in
+// block order, divides by the image's norm and adds the bias (bitwise repeatable, no atomics).  With
+// out == nullptr only the scores leave the kernel (the FV is never written to HBM).
 constexpr int kFinKR = 2;  // dims per thread (kr, kr + 32)
 __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
   __shared__ double s_red[8];
+  __shared__ float s_dot[8][kMaxCls];
   __shared__ int s_last;
   const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, jq = tid & 7, kr = (tid >> 3) + kDP * (int)blockIdx.z;
   const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
@@ -402,13 +415,51 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
     }
   }
   __syncthreads();
-  float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D + kb;
-  for (int t = tid; t < nj * nk; t += 256) {
-    const int r = t / nk, k = t - r * nk;
-    o[(size_t)r * p.D + k] = sU[r][k];
-    o[KD + (size_t)r * p.D + k] = sV[r][k];
+  const int part = blockIdx.z * gridDim.x + blockIdx.x, nparts = gridDim.x * gridDim.z;
+  if (p.out) {
+    float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D + kb;
+    for (int t = tid; t < nj * nk; t += 256) {
+      const int r = t / nk, k = t - r * nk;
+      o[(size_t)r * p.D + k] = sU[r][k];
+      o[KD + (size_t)r * p.D + k] = sV[r][k];
+    }
   }
-  if (p.mode == 2) return;
+  if (p.n_cls > 0) {
+    // this thread's tile elements t = tid + 256 u (nj * nk <= 2048), classifier reads coalesced over t
+    constexpr int kE = kFinJ * kDP / 256;
+    float zu[kE], zv[kE];
+    int wo[kE];
+#pragma unroll
+    for (int u = 0; u < kE; ++u) {
+      const int t = tid + 256 * u, r = t / nk, k = t - r * nk;
+      const bool ok = t < nj * nk;
+      zu[u] = ok ? sU[r][k] : 0.f;
+      zv[u] = ok ? sV[r][k] : 0.f;
+      wo[u] = ok ? r * p.D + k : 0;
+    }
+    const float *wb = p.svm_w + (size_t)j0 * p.D + kb;
+    for (int c = 0; c < p.n_cls; ++c) {
+      const float *wc = wb + (size_t)c * 2 * KD;
+      float a = 0.f;
+#pragma unroll
+      for (int u = 0; u < kE; ++u) {
+        a = fmaf(zu[u], __ldg(wc + wo[u]), a);
+        a = fmaf(zv[u], __ldg(wc + KD + wo[u]), a);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if ((tid & 31) == 0) s_dot[tid >> 5][c] = a;
+    }
+    __syncthreads();
+    if (tid < p.n_cls) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += (double)s_dot[w][tid];
+      p.spart[((size_t)b * kFinMaxParts + part) * p.n_cls + tid] = t;  // own slot: no atomics
+      __threadfence();
+    }
+  }
+  const bool l2 = p.mode != 2;
+  if (!l2 && p.n_cls == 0) return;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
   if ((tid & 31) == 0) s_red[tid >> 5] = ss;
@@ -416,17 +467,24 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   if (tid == 0) {
     double tot = 0.0;
     for (int w = 0; w < 8; ++w) tot += s_red[w];
-    p.norm2[(size_t)b * kFinMaxParts + blockIdx.z * gridDim.x + blockIdx.x] = tot;  // own slot: no atomics
+    p.norm2[(size_t)b * kFinMaxParts + part] = tot;  // own slot: no atomics
     __threadfence();
     const unsigned ticket = atomicAdd(p.counters + b, 1u);  // only decides which block is last
-    s_last = (ticket == gridDim.x * gridDim.z - 1);
+    s_last = (ticket == nparts - 1);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   double n2 = 0.0;  // fixed-order sum of the parts: bitwise repeatable
-  for (unsigned k = 0; k < gridDim.x * gridDim.z; ++k) n2 += __ldcg(p.norm2 + (size_t)b * kFinMaxParts + k);
-  if (!(n2 > 0.0)) return;
+  if (l2)
+    for (int k = 0; k < nparts; ++k) n2 += __ldcg(p.norm2 + (size_t)b * kFinMaxParts + k);
+  if (tid < p.n_cls) {  // scores of the normalised FV (an all-zero FV scores the bias)
+    double d = 0.0;
+    for (int k = 0; k < nparts; ++k) d += __ldcg(p.spart + ((size_t)b * kFinMaxParts + k) * p.n_cls + tid);
+    const double inv = l2 ? (n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0) : 1.0;
+    p.scores[(size_t)b * p.n_cls + tid] = (float)(d * inv + (p.svm_b ? (double)p.svm_b[tid] : 0.0));
+  }
+  if (!l2 || !p.out || !(n2 > 0.0)) return;
   const float sc = (float)(1.0 / sqrt(n2));
   float4 *ob = reinterpret_cast<float4 *>(p.out + (size_t)b * 2 * KD);  // 2KD % 4 == 0 (D % 4 == 0)
   const int n4 = (2 * KD) / 4;

@@ -90,3 +90,30 @@ def test_status_strings(lib):
 def test_python_binding_imports_without_gpu():
     import paper_1604_03498_b200 as fv
     assert fv.lib_path.endswith("libgpufv.so") and fv.lib.fv_version() >= 1
+
+
+def _scored(lib, n_cls=2, w=1, scores=1, K=16, D=64):
+    f = lib.fv_encode_scored_batched
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_uint, ctypes.c_void_p,
+                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                  ctypes.c_void_p]
+    p = lambda v: ctypes.c_void_p(v * 4096) if v else None
+    return f(p(1), p(1), 1, 10, D, p(1), p(1), p(1), K, 0.0, 0, p(w), None, n_cls, p(scores), None, p(1), 1 << 30,
+             None)
+
+
+@pytest.mark.parametrize("kw", [dict(n_cls=0), dict(n_cls=33), dict(w=0), dict(scores=0)])
+def test_scored_argument_validation(lib, kw):
+    assert _scored(lib, **kw) == 1
+
+
+def test_scored_workspace_grows_with_classes(lib):
+    f = lib.fv_workspace_bytes_scored
+    f.restype = ctypes.c_size_t
+    f.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint]
+    # no device here: the layout query may fail (0); when it works, more classes need more room
+    a, b = f(10000, 100, 256, 64, 1, 0, 0), f(10000, 100, 256, 64, 32, 0, 0)
+    assert (a == 0 and b == 0) or b > a
+    assert f(10000, 100, 256, 64, 0, 0, 0) == 0 and f(10000, 100, 256, 64, 33, 0, 0) == 0
