@@ -14,9 +14,11 @@ from .oracle import (  # noqa: F401
     NORM_POWER_L2,
     accumulate,
     build,
+    em_step,
     encode,
     encode_batched,
     fv_from_stats,
+    loglik_rows,
     max_threads,
     normalize,
     posteriors,

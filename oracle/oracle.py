@@ -199,3 +199,51 @@ def score(fv, W, bias=None) -> np.ndarray:
     if bias is not None:
         s = s + _d(bias)[None, :]
     return s if fv.ndim == 2 else s[0]
+
+
+# ------------------------------------------------------------------ GMM EM training (NEXT-3)
+# "the GMM components trained beforehand" — standard EM for a diagonal GMM,
+# with SPEC's train_gmm floors: variance floor max(abs, rel * global per-dim variance), prior
+# floor with renormalisation.  Plain numpy in float64; posteriors from the C oracle above.
+
+def loglik_rows(X, priors, means, variances) -> np.ndarray:
+    """Per-descriptor log-likelihood ln sum_j pi_j N(x_i; mu_j, diag var_j) (natural log, including the
+    -(D/2) ln 2 pi constant): l_ij = ln pi_j - 1/2 sum_k ln(2 pi var_jk) - 1/2 sum_k (x_ik - mu_jk)^2 / var_jk
+    (direct form, reading A2), then max + ln sum exp(l - max) per row (Alg.1 l.6-14's maxPost/sum)."""
+    w, m, v, K, D = _gmm(priors, means, variances)
+    X = _d(X).reshape(-1, D)
+    L = np.empty((X.shape[0], K))
+    for j in range(K):
+        L[:, j] = (np.log(w[j]) - 0.5 * np.sum(np.log(2.0 * np.pi * v[j]))
+                   - 0.5 * np.sum((X - m[j]) ** 2 / v[j], axis=1))
+    mx = L.max(axis=1)
+    return mx + np.log(np.exp(L - mx[:, None]).sum(axis=1))
+
+
+def em_step(X, priors, means, variances, var_floor_abs: float = 1e-6, var_floor_rel: float = 1e-4,
+            prior_floor: float = 1e-8):
+    """One EM iteration.  Returns (priors', means', variances', LL) where LL = sum_i ln p(x_i) under the
+    INPUT model.  E-step: gamma (Alg.1 Phase 1).  M-step (two-pass, plain definitions):
+      N_j = sum_i gamma_ij;  mu_j = sum_i gamma_ij x_i / N_j;  var_jk = sum_i gamma_ij (x_ik - mu_jk)^2 / N_j
+      var_jk <- max(var_jk, max(var_floor_abs, var_floor_rel * var_k(X)))   (var_k(X): biased, all rows)
+      pi_j = max(N_j / N, prior_floor), then pi /= sum pi
+    A component with N_j == 0 keeps its mean and (floored) variance (reading A20)."""
+    w, m, v, K, D = _gmm(priors, means, variances)
+    X = _d(X).reshape(-1, D)
+    N = X.shape[0]
+    g = posteriors(X, w, m, v)
+    LL = float(loglik_rows(X, w, m, v).sum())
+    Nj = g.sum(axis=0)
+    mu = m.copy()
+    var = v.copy()
+    for j in range(K):
+        if Nj[j] > 0:
+            mu[j] = (g[:, j:j + 1] * X).sum(axis=0) / Nj[j]
+            var[j] = (g[:, j:j + 1] * (X - mu[j]) ** 2).sum(axis=0) / Nj[j]
+    gmean = X.sum(axis=0) / N
+    gvar = ((X - gmean) ** 2).sum(axis=0) / N
+    floor = np.maximum(var_floor_abs, var_floor_rel * gvar)
+    var = np.maximum(var, floor[None, :])
+    pi = np.maximum(Nj / N, prior_floor)
+    pi = pi / pi.sum()
+    return pi, mu, var, LL

@@ -347,3 +347,80 @@ def test_score_self_similarity_basis_and_linearity():
     np.testing.assert_allclose(oracle.score(F, 2 * W1 - W2, b), 2 * oracle.score(F, W1) - oracle.score(F, W2) + b,
                                rtol=1e-12, atol=1e-12)
     assert oracle.score(F[1], W1).shape == (2,)
+
+
+# ---------------------------------------------------------------- GMM EM (NEXT-3)
+def test_loglik_matches_scipy_mixture_density():
+    """ln p(x) against scipy's multivariate normal log-pdf (diagonal covariance) + logsumexp: a library
+    path with its own normalising constants (pins the -(D/2) ln 2 pi, log-det and prior terms)."""
+    from scipy.special import logsumexp
+    from scipy.stats import multivariate_normal
+    gmm = fvgen.make_gmm(5, 4, seed=41)
+    X = fvgen.make_descriptors(gmm, 200, seed=42).astype(np.float64)
+    pi, mu, var = (a.astype(np.float64) for a in gmm)
+    comp = np.stack([np.log(pi[j]) + multivariate_normal(mu[j], np.diag(var[j])).logpdf(X) for j in range(5)], 1)
+    np.testing.assert_allclose(oracle.loglik_rows(X, *gmm), logsumexp(comp, axis=1), rtol=1e-12, atol=1e-10)
+
+
+def test_em_single_component_is_sample_mean_and_variance():
+    """K=1: one M-step gives the sample mean and biased sample variance (numpy routines), pi = 1, and
+    LL = sum of univariate normal log-pdfs (scipy) under the input model (SPEC train_gmm N=1 example)."""
+    from scipy.stats import norm
+    rng = np.random.default_rng(43)
+    X = rng.normal(size=(500, 3)) * [1.0, 0.5, 2.0] + [0.3, -1.0, 4.0]
+    mu0, var0 = np.array([[0.0, 0.0, 1.0]]), np.array([[2.0, 1.0, 3.0]])
+    pi, mu, var, LL = oracle.em_step(X, [1.0], mu0, var0)
+    np.testing.assert_allclose(pi, [1.0], rtol=0, atol=0)
+    np.testing.assert_allclose(mu[0], X.mean(axis=0), rtol=1e-13)
+    np.testing.assert_allclose(var[0], X.var(axis=0), rtol=1e-12)
+    assert LL == pytest.approx(norm.logpdf(X, mu0[0], np.sqrt(var0[0])).sum(), rel=1e-13)
+
+
+def test_em_mstep_equals_weighted_moments():
+    """M-step = posterior-weighted mean / biased covariance diagonal (np.average, np.cov aweights) and
+    pi = mean posterior — library routines on the oracle's own gamma."""
+    gmm = fvgen.make_gmm(6, 5, seed=44)
+    X = fvgen.make_descriptors(gmm, 800, seed=45).astype(np.float64)
+    pi, mu, var, _ = oracle.em_step(X, *gmm, var_floor_abs=0.0, var_floor_rel=0.0, prior_floor=0.0)
+    g = oracle.posteriors(X, *gmm)
+    for j in range(6):
+        np.testing.assert_allclose(mu[j], np.average(X, axis=0, weights=g[:, j]), rtol=1e-11, atol=1e-13)
+        np.testing.assert_allclose(var[j], np.diag(np.cov(X.T, aweights=g[:, j], bias=True)), rtol=1e-10)
+    np.testing.assert_allclose(pi, g.mean(axis=0), rtol=1e-12)
+    assert pi.sum() == pytest.approx(1.0, abs=1e-14)
+
+
+def test_em_monotone_loglik_and_separated_clusters():
+    """EM never decreases the log-likelihood (SPEC: non-decreasing within 1e-8), and two well separated
+    clusters are recovered from a perturbed start (means within 0.1 of the true centres)."""
+    rng = np.random.default_rng(46)
+    c = np.array([[-5.0, 0.0, 2.0], [5.0, 1.0, -2.0]])
+    X = np.concatenate([c[0] + rng.normal(size=(400, 3)), c[1] + 0.5 * rng.normal(size=(600, 3))])
+    pi, mu, var = np.array([0.5, 0.5]), c + [[1.0, -1.0, 0.5], [-1.0, 0.5, 1.0]], np.ones((2, 3)) * 4.0
+    lls = []
+    for _ in range(12):
+        pi, mu, var, LL = oracle.em_step(X, pi, mu, var)
+        lls.append(LL)
+    assert all(b >= a - 1e-8 * abs(a) for a, b in zip(lls, lls[1:]))
+    assert np.abs(mu - c).max() < 0.1
+    np.testing.assert_allclose(pi, [0.4, 0.6], atol=1e-6)
+
+
+def test_em_floors_and_component_permutation():
+    """Variance floor (max(abs, rel * global var)) binds for a component sitting on duplicate points;
+    the prior floor keeps a far component's weight at ~1e-8 after renormalisation; permuting the
+    components permutes the result."""
+    rng = np.random.default_rng(47)
+    X = np.concatenate([np.tile([[1.0, 2.0]], (50, 1)), rng.normal(size=(300, 2))])
+    mu0 = np.array([[1.0, 2.0], [0.0, 0.0], [1e3, 1e3]])
+    var0 = np.array([[1e-4, 1e-4], [1.0, 1.0], [1.0, 1.0]])
+    pi, mu, var, _ = oracle.em_step(X, [0.2, 0.7, 0.1], mu0, var0, var_floor_abs=1e-6, var_floor_rel=1e-3)
+    gvar = X.var(axis=0)
+    np.testing.assert_allclose(var[0], 1e-3 * gvar, rtol=1e-12)
+    assert pi[2] == pytest.approx(1e-8 / (1 + 1e-8), rel=1e-6)
+    perm = [2, 0, 1]
+    pp, mp_, vp, LLp = oracle.em_step(X, np.array([0.2, 0.7, 0.1])[perm], mu0[perm], var0[perm],
+                                      var_floor_abs=1e-6, var_floor_rel=1e-3)
+    np.testing.assert_allclose(pp, pi[perm], rtol=1e-12)
+    np.testing.assert_allclose(mp_, mu[perm], rtol=1e-12)
+    np.testing.assert_allclose(vp, var[perm], rtol=1e-12)
