@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--score-steps", type=int, default=5,
                     help="steps of the fused-scoring monitoring leg (NEXT-4; 0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="wall budget of the oracle sample")
-    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5", "em"],
                     help="c4: frame-sharded stream (default, the metric's config); c5: one 10M x 128 set, K=512, "
                          "descriptor-sharded with an NCCL all-reduce of the fp64 statistics")
     ap.add_argument("--c5-n", type=int, default=10_000_000, help="C5 set size (all ranks together)")
@@ -384,6 +384,113 @@ def run_c5(args, rank, world, local):
         torch.distributed.destroy_process_group()
 
 
+def run_em(args, rank, world, local):
+    """GMM EM training: one EM iteration = E-step (exact posteriors,
+    sufficient statistics and log-likelihood through the production stats kernel) + M-step, over the
+    C3-sized descriptor pool (256 images x 20,000 = 5.12 M descriptors per rank, K=256, D=64), started
+    from a different seeded GMM.  Multi-GPU: descriptor-sharded, one all_reduce of the 1+K(2D+1)+1 fp64
+    values per iteration (dist.em_step_sharded), weak scaling."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1604_03498_b200 as fv
+    from paper_1604_03498_b200 import dist as fvdist
+    n_frames = 256 * 4  # 1024 blocks of 5000 = 5.12 M rows
+    true_np = fvgen.make_gmm(K, D, seed=1604)
+    X = fvgen.make_frames(true_np, n_frames, PER_FRAME, seed=1604 + 30000 + rank * 1_000_003).reshape(-1, D)
+    n = X.shape[0]
+    init_np = fvgen.make_gmm(K, D, seed=1704)
+    Xd = torch.from_numpy(X).to(dev)
+    ws = fv.Workspace(device=dev)
+    ws.ensure(int(fv.lib.fv_workspace_bytes_em(n, K, D, 0)))
+    stream = torch.cuda.current_stream(dev)
+    g_init = fv.GMM(*init_np, device=dev)
+    g_a = fv.GMM(*init_np, device=dev)
+    lls = []
+
+    def step():
+        # one EM iteration from the fixed init (every step does identical work)
+        g_a.weights.copy_(g_init.weights); g_a.means.copy_(g_init.means); g_a.sigmas.copy_(g_init.sigmas)
+        g_a.flags = 0
+        if world > 1:
+            new, ll = fvdist.em_step_sharded(Xd, g_a, estep_fn=lambda Xs: fv.gmm_estep(Xs, g_a, ws=ws),
+                                             mstep_fn=lambda st: fv.gmm_mstep(st, g_a, ws=ws))
+            lls.append(ll)
+        else:
+            fv.gmm_em_step(Xd, g_a, ws=ws, out=g_a)
+
+    step()
+    torch.cuda.synchronize(dev)
+    parity = None
+    if rank == 0:  # a 20k-row sample through the same entry point vs the oracle's EM step
+        import oracle
+        m = 20000
+        new, ll = fv.gmm_em_step(Xd[:m].contiguous(), fv.GMM(*init_np, device=dev))
+        pi_r, mu_r, var_r, ll_r = oracle.em_step(X[:m], *init_np)
+        err_mu = float(np.max(np.abs(new.means.cpu().numpy() - mu_r) / np.sqrt(var_r)))
+        err_ll = abs(float(ll.item()) - ll_r) / m
+        parity = {"sample_rows": m, "max_mu_err_over_sd": err_mu, "loglik_err_per_desc": err_ll,
+                  "tolerance": {"mu_over_sd": 1e-3, "loglik_per_desc": 2e-5}}
+        if err_ll > 2e-5:
+            raise SystemExit(f"EM parity failure before timing: {parity}")
+    clk = ClockSampler(local, pci_bus_id(dev)).__enter__()
+    for _ in range(max(3, args.warmup)):
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clk.mark_start()
+    try:
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    finally:
+        clk.mark_stop()
+        clk.__exit__(None, None, None)
+    total_ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_seconds > 0:
+        import oracle
+        m = 4000
+        t = time.perf_counter()
+        oracle.em_step(X[:m], *init_np)
+        dt = time.perf_counter() - t
+        cpu = {"value": m / dt, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+               "sample": f"one oracle EM step (C posteriors + numpy M-step) on {m} rows ({dt:.1f} s wall)"}
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    peak_tf, peak_src = tensor_peak()
+    achieved = FLOP_PER_DESC * n / (ms * 1e-3) / 1e12
+    line = {
+        "metric": f"descriptors/sec per GMM EM iteration (K={K},D={D})", "value": world * n / (ms * 1e-3),
+        "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+        "config": {"workload": f"EM iteration on {n} descriptors per rank (C3-sized pool), K={K}, D={D}, exact "
+                               "posteriors, from a seeded init", "parallelism": f"descriptor-sharded x{world}"
+                               + (", all_reduce of stats + loglik" if world > 1 else "")},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tf, "traffic": None, "kernel": "k_stats (whole EM step timed)",
+                     "flop_per_desc": FLOP_PER_DESC, "peak_source": peak_src},
+        "clocks": clk.summary(), "gpu_launches": None, "parity": parity, "cpu_baseline": cpu, "e2e": None,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -392,6 +499,9 @@ def main():
         return
     if args.workload == "c5":
         run_c5(args, rank, world, local)
+        return
+    if args.workload == "em":
+        run_em(args, rank, world, local)
         return
     import torch
     torch.cuda.set_device(local)

@@ -25,7 +25,9 @@
  *     D <= 64 runs the narrow kernel (128 Gaussians per CTA); 64 < D <= 128 the wide one (64 per CTA).
  *   - Device data is not validated (that would need a kernel + sync): var <= 0, pi <= 0 or non-finite
  *     X propagate NaN into that image's output only.  Descriptors with |x-c|/rms >= 255 in some
- *     dimension (c, rms: GMM-weighted mean/RMS) overflow the fp16 split operands.
+ *     dimension (c, rms: GMM-weighted mean/RMS) overflow the fp16 split operands, and
+ *     so does a component whose standard deviation in some dimension is below ~rms/150 (its
+ *     -1/(2 var) coefficient exceeds the fp16 range); both give NaN/inf for the affected images.
  *   - Synchronous argument errors return a status; asynchronous CUDA errors are reported by the
  *     next call or by cudaGetLastError.  fv_last_error() returns a thread-local detail string.
  *   - Thread safety: reentrant; concurrent calls need distinct workspaces.
@@ -139,6 +141,40 @@ fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, in
 fv_status fv_finalize(const double *stats, int batch, int D, const float *weights, const float *means,
                       const float *sigmas, int K, unsigned flags, float *out, void *ws, size_t ws_bytes,
                       fv_stream_t stream);
+
+/* GMM training by EM on the GPU ("the GMM components trained beforehand",
+ * P:141-142).  The E-step reuses the production path: exact posteriors (threshold 0) from the
+ * GEMM1 + softmax kernel, sufficient statistics from GEMM2, plus each descriptor's log-likelihood.
+ *
+ * fv_gmm_estep: one descriptor set X (N x D) under the GMM (w, mu, sg) ->
+ *   stats   (device, 1 + K(2D+1) doubles) = [N, S0 (K), S1 (K x D), S2 (K x D)] about c (as
+ *           fv_stats_batched with threshold 0; they add across descriptor shards),
+ *   loglik  (device, 1 double) = sum_i ln sum_j pi_j N(x_i; mu_j, diag var_j) (natural log, with the
+ *           -(D/2) ln 2 pi constant; also additive across shards).
+ * fv_gmm_mstep: stats (possibly summed over ranks) -> new parameters (device, fp32; variances
+ *   whatever the sigma convention of the input), with SPEC train_gmm's floors:
+ *     mu_j = c + S1_j/S0_j,  var_j = max(S2_j/S0_j - (S1_j/S0_j)^2, max(var_floor_abs, var_floor_rel * var_k(X))),
+ *     pi_j = max(S0_j/N, prior_floor) / sum_l max(S0_l/N, prior_floor)
+ *   where var_k(X) is the data's biased per-dimension variance (from the same statistics).  A component
+ *   with S0_j == 0 keeps its mean and variance (reading A20).  The outputs may alias the inputs.
+ *   Precision: the moment form about c turns the fp32 statistics' ~1e-7 relative error into an absolute
+ *   variance error of ~1e-6 (|mu_j - c|^2 + var_j) (tests/test_gpu_em.py).
+ *   Uses the prepared GMM (c) in ws: runs a1 unless FV_PREPARED.
+ * fv_gmm_em_step: both on one device (stats kept in ws); loglik is the INPUT model's.
+ * Floors must be finite and >= 0, prior_floor < 1 (else FV_ERR_ARG); EM needs N >= 1.
+ * ws >= fv_workspace_bytes_em(N, K, D, flags). */
+size_t fv_workspace_bytes_em(int64_t N, int K, int D, unsigned flags);
+fv_status fv_gmm_estep(const float *X, int64_t N, int D, const float *weights, const float *means,
+                       const float *sigmas, int K, unsigned flags, double *stats, double *loglik, void *ws,
+                       size_t ws_bytes, fv_stream_t stream);
+fv_status fv_gmm_mstep(const double *stats, int D, const float *weights, const float *means, const float *sigmas,
+                       int K, unsigned flags, float var_floor_abs, float var_floor_rel, float prior_floor,
+                       float *new_weights, float *new_means, float *new_vars, void *ws, size_t ws_bytes,
+                       fv_stream_t stream);
+fv_status fv_gmm_em_step(const float *X, int64_t N, int D, const float *weights, const float *means,
+                         const float *sigmas, int K, unsigned flags, float var_floor_abs, float var_floor_rel,
+                         float prior_floor, float *new_weights, float *new_means, float *new_vars, double *loglik,
+                         void *ws, size_t ws_bytes, fv_stream_t stream);
 
 /* Test hook: posteriors gamma (N x K fp32) of one set, computed by the production kernel (same
  * GEMM + softmax path as fv_encode); entries <= threshold are zeroed when threshold > 0. */

@@ -16,7 +16,8 @@ __all__ = [
     "NORM_IMPROVED", "NORM_POWER_L2", "NORM_NONE", "SIGMA_IS_STDDEV", "PREPARED",
     "GMM", "Workspace", "lib", "lib_path", "workspace_bytes", "gmm_prepare", "encode", "encode_batched",
     "encode_batched_host", "stats_batched", "finalize", "posteriors", "last_launch_count", "profile_events",
-    "encode_scored_batched", "encode_scored_batched_host", "MAX_CLASSES", "FVError",
+    "encode_scored_batched", "encode_scored_batched_host", "MAX_CLASSES", "gmm_estep", "gmm_mstep", "gmm_em_step",
+    "gmm_fit", "FVError",
 ]
 
 NORM_IMPROVED = 0
@@ -58,6 +59,14 @@ lib.fv_encode_scored_batched.argtypes = [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _
                                          _vp, _vp, _vp, _sz, _vp]
 lib.fv_encode_scored_batched_host.argtypes = [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _i32, _f32, _u32, _vp, _vp,
                                               _i32, _vp, _vp, _sz, _vp]
+lib.fv_workspace_bytes_em.argtypes = [_i64, _i32, _i32, _u32]
+lib.fv_workspace_bytes_em.restype = _sz
+lib.fv_gmm_estep.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _u32, _vp, _vp, _vp, _sz, _vp]
+lib.fv_gmm_mstep.argtypes = [_vp, _i32, _vp, _vp, _vp, _i32, _u32, _f32, _f32, _f32, _vp, _vp, _vp, _vp, _sz, _vp]
+lib.fv_gmm_em_step.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _u32, _f32, _f32, _f32, _vp, _vp, _vp, _vp, _vp,
+                               _sz, _vp]
+for _fn in ("fv_gmm_estep", "fv_gmm_mstep", "fv_gmm_em_step"):
+    getattr(lib, _fn).restype = _i32
 for _fn in ("fv_gmm_prepare", "fv_encode", "fv_encode_batched", "fv_encode_batched_host", "fv_stats_batched",
             "fv_finalize", "fv_posteriors", "fv_encode_scored_batched", "fv_encode_scored_batched_host"):
     getattr(lib, _fn).restype = _i32
@@ -325,3 +334,69 @@ def encode_scored_batched_host(X_host, offsets_host, gmm: GMM, svm_w, svm_b=None
                                              gmm.K, float(threshold), _mode_flags(gmm, mode, prepared), _ptr(W),
                                              _ptr(svm_b), n_cls, _ptr(scores_host), *ws.args(), _stream()))
     return scores_host
+
+
+# ------------------------------------------------------------------ GMM EM training (NEXT-3)
+def _em_ws(ws, N, gmm, device):
+    need = int(lib.fv_workspace_bytes_em(int(N), gmm.K, gmm.D, 0))
+    if need == 0:
+        raise FVError(1)
+    return _ws(ws, need, device)[0]
+
+
+def gmm_estep(X, gmm: GMM, ws: Workspace | None = None):
+    """E-step (P:141-142): (stats (1 + K(2D+1),) float64 about c, loglik (1,) float64) of X under gmm;
+    both add across descriptor shards."""
+    _check_X(X, gmm.D)
+    ws = _em_ws(ws, X.shape[0], gmm, X.device)
+    st = torch.empty(1 + gmm.K * (2 * gmm.D + 1), dtype=torch.float64, device=X.device)
+    ll = torch.empty(1, dtype=torch.float64, device=X.device)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_gmm_estep(_ptr(X), X.shape[0], gmm.D, w, m, s, gmm.K, gmm.flags, _ptr(st), _ptr(ll), *ws.args(),
+                            _stream()))
+    return st, ll
+
+
+def gmm_mstep(stats, gmm: GMM, var_floor_abs: float = 1e-6, var_floor_rel: float = 1e-4,
+              prior_floor: float = 1e-8, ws: Workspace | None = None) -> GMM:
+    """M-step from (possibly all-reduced) E-step statistics -> a new GMM (variances)."""
+    assert stats.is_cuda and stats.dtype == torch.float64 and stats.is_contiguous()
+    ws = _em_ws(ws, 0, gmm, stats.device)
+    new = GMM(torch.empty_like(gmm.weights), torch.empty_like(gmm.means), torch.empty_like(gmm.sigmas),
+              device=gmm.means.device)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_gmm_mstep(_ptr(stats), gmm.D, w, m, s, gmm.K, gmm.flags, float(var_floor_abs), float(var_floor_rel),
+                            float(prior_floor), *new.ptrs(), *ws.args(), _stream()))
+    return new
+
+
+def gmm_em_step(X, gmm: GMM, var_floor_abs: float = 1e-6, var_floor_rel: float = 1e-4, prior_floor: float = 1e-8,
+                ws: Workspace | None = None, out: GMM | None = None):
+    """One EM iteration on one device -> (new GMM, loglik of X under the INPUT gmm as a (1,) float64
+    tensor).  ``out`` may be ``gmm`` itself (in-place update)."""
+    _check_X(X, gmm.D)
+    ws = _em_ws(ws, X.shape[0], gmm, X.device)
+    if out is None:
+        out = GMM(torch.empty_like(gmm.weights), torch.empty_like(gmm.means), torch.empty_like(gmm.sigmas),
+                  device=gmm.means.device)
+    ll = torch.empty(1, dtype=torch.float64, device=X.device)
+    w, m, s = gmm.ptrs()
+    _check(lib.fv_gmm_em_step(_ptr(X), X.shape[0], gmm.D, w, m, s, gmm.K, gmm.flags, float(var_floor_abs),
+                              float(var_floor_rel), float(prior_floor), *out.ptrs(), _ptr(ll), *ws.args(), _stream()))
+    out.flags = 0  # the M-step writes variances
+    return out, ll
+
+
+def gmm_fit(X, init: GMM, max_iters: int = 100, tol: float = 1e-6, **floors):
+    """EM from ``init`` until the relative log-likelihood improvement is < tol (SPEC train_gmm S:255) or
+    max_iters.  Returns (GMM, [loglik per iteration]).  Host loop only; every step runs in the kernels
+    (one device sync per iteration to read the log-likelihood)."""
+    ws = Workspace(device=X.device)
+    cur, hist = init, []
+    for _ in range(max_iters):
+        nxt, ll = gmm_em_step(X, cur, ws=ws, **floors)
+        hist.append(float(ll.item()))
+        cur = nxt
+        if len(hist) > 1 and abs(hist[-1] - hist[-2]) <= tol * abs(hist[-2]):
+            break
+    return cur, hist

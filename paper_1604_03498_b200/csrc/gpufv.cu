@@ -94,14 +94,15 @@ int num_clusters(int C, bool wide) {
 struct Layout {
   int C, Kp, ncl, dpad;  // cluster size, padded K, clusters, padded D (64 | 128)
   int64_t n_total, nslots;                                         // segment slots (cluster, image)
-  size_t wimg, bias, xshift, xscale, cshift, bscratch, coef;  // prepared GMM (head of ws)
+  size_t wimg, bias, xshift, xscale, cshift, bscratch, bmax, coef;  // prepared GMM (head of ws)
   size_t tiles, off1, cstart, cown, norm2, s0slots, slots;  // per call
   size_t spart;                                           // fused scoring partial dots (n_cls > 0)
+  size_t llrows, llparts, emstats;                        // EM: per-row log2-likelihoods, reduction, stats
   size_t hx, hoff, hout;                                  // _host entry point
   size_t total;
 };
 
-bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout &L, int n_cls = 0) {
+bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout &L, int n_cls = 0, bool em = false) {
   L.C = cluster_size(K, D);
   L.Kp = L.C * gauss_per_cta(K, D);
   L.dpad = is_wide(K, D) ? kDMax : kDP;
@@ -120,7 +121,8 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.xshift = o;   o = align_up(o + kDMax * 4, 256);
   L.xscale = o;   o = align_up(o + kDMax * 4, 256);
   L.cshift = o;   o = align_up(o + kDMax * 8, 256);
-  L.bscratch = o; o = align_up(o + (size_t)L.Kp * 8, 1024);
+  L.bscratch = o; o = align_up(o + (size_t)L.Kp * 8, 256);
+  L.bmax = o;     o = align_up(o + 8, 1024);
   L.coef = o;     o = align_up(o + (size_t)3 * kDMax * L.Kp * 8, 1024);
   L.tiles = o;    o = align_up(o + (size_t)(batch + 1) * 8, 256);
   L.off1 = o;     o = align_up(o + 16, 256);
@@ -130,6 +132,12 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * 4 * L.Kp * 4, 1024);
   L.slots = o;    o = align_up(o + (size_t)L.nslots * 2 * L.dpad * L.Kp * 4, 1024);
   L.spart = o;    o = align_up(o + (size_t)(n_cls > 0 ? batch : 0) * kFinMaxParts * n_cls * 8, 1024);
+  L.llrows = L.llparts = L.emstats = o;
+  if (em) {
+    L.llrows = o;  o = align_up(o + (size_t)n_total * 4, 1024);
+    L.llparts = o; o = align_up(o + (size_t)kLLBlocks * 8 + 8, 1024);  // block slots + ticket
+    L.emstats = o; o = align_up(o + ((size_t)1 + (size_t)K * (2 * D + 1)) * 8, 1024);
+  }
   L.hx = L.hoff = L.hout = 0;
   if (host_io) {
     // device staging of X, offsets and the per-image result (scores when n_cls > 0, else FVs)
@@ -179,7 +187,8 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
                       void *ws, cudaStream_t st) {
   const int sd = (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0;
   k_prep_shift<<<1, 256, 0, st>>>(w, mu, sg, K, D, L.Kp, sd, (double *)at(ws, L.cshift), (float *)at(ws, L.xshift),
-                                  (float *)at(ws, L.xscale), (float *)at(ws, L.bias), (double *)at(ws, L.bscratch));
+                                  (float *)at(ws, L.xscale), (float *)at(ws, L.bias), (double *)at(ws, L.bscratch),
+                                  (double *)at(ws, L.bmax));
   k_prep_w<<<L.Kp, 2 * L.dpad, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
                                  at(ws, L.wimg), (double *)at(ws, L.coef), is_wide(K, D) ? 1 : 0);
   g_launches += 2;
@@ -188,7 +197,8 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
 
 // a2-a6 over a batch: schedule + persistent stats kernel.  gamma (optional) for fv_posteriors.
 fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets, int64_t n_single, int batch, int D,
-                       int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st) {
+                       int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st,
+                       float *loglik_rows = nullptr) {
   // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
   int64_t *off1 = (int64_t *)at(ws, L.off1);
   k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles), L.ncl,
@@ -206,6 +216,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.slots = (float *)at(ws, L.slots);
   p.s0slots = (float *)at(ws, L.s0slots);
   p.gamma_out = gamma;
+  p.loglik_out = loglik_rows;
   p.trace = g_trace;
   p.batch = batch;
   p.D = D;
@@ -588,6 +599,114 @@ fv_status fv_posteriors(const float *X, int64_t N, int D, const float *w, const 
   if (N == 0) return FV_OK;
   const int64_t *offs = nullptr;
   return launch_stats(L, X, offs, N, 1, D, K, thr, ws, gamma, mode, st);
+}
+
+size_t fv_workspace_bytes_em(int64_t N, int K, int D, unsigned flags) {
+  (void)flags;
+  Layout L;
+  if (K < 1 || K > kMaxK || N < 0) return 0;
+  if (!make_layout(N, 1, K, D, false, L, 0, true)) return 0;
+  return L.total;
+}
+
+}  // extern "C"
+
+namespace {
+
+// E-step of EM (NEXT-3) on one descriptor set: exact posteriors through the production stats kernel,
+// sufficient statistics [N, S0, S1, S2] about c (k_reduce_stats) and the total log-likelihood.
+fv_status estep_impl(const Layout &L, const float *X, int64_t N, int D, const float *w, const float *mu,
+                     const float *sg, int K, unsigned flags, double *stats, double *loglik, void *ws, cudaStream_t st) {
+  if (!(flags & FV_PREPARED))
+    if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
+  const size_t nst = (1 + (size_t)K * (2 * D + 1)) * 8;
+  if (N == 0) {
+    if (cudaMemsetAsync(stats, 0, nst, st) != cudaSuccess || cudaMemsetAsync(loglik, 0, 8, st) != cudaSuccess)
+      return cuda_check("memset");
+    return FV_OK;
+  }
+  const int64_t *offs = nullptr;
+  float *llrows = (float *)at(ws, L.llrows);
+  if (fv_status s = launch_stats(L, X, offs, N, 1, D, K, 0.f, ws, nullptr, 0, st, llrows)) return s;
+  FinParams f = fin_params(L, offs, 1, K, D, w, mu, sg, flags, ws);
+  f.stats_out = stats;
+  k_reduce_stats<<<dim3((K + kFinJ - 1) / kFinJ, 1, (D + kDP - 1) / kDP), 256, 0, st>>>(f);
+  double *parts = (double *)at(ws, L.llparts);
+  unsigned *ticket = (unsigned *)(parts + kLLBlocks);
+  if (cudaMemsetAsync(ticket, 0, 4, st) != cudaSuccess) return cuda_check("memset ticket");
+  k_loglik_reduce<<<kLLBlocks, 256, 0, st>>>(llrows, N, D, (const double *)at(ws, L.bmax), parts, ticket, loglik);
+  g_launches += 2;
+  return cuda_check("k_reduce_stats/k_loglik_reduce");
+}
+
+fv_status mstep_impl(const Layout &L, const double *stats, int D, const float *w, const float *mu, const float *sg,
+                     int K, unsigned flags, float floor_abs, float floor_rel, float prior_floor, float *w_new,
+                     float *mu_new, float *var_new, void *ws, cudaStream_t st) {
+  if (!(flags & FV_PREPARED))
+    if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
+  k_mstep<<<1, 1024, 0, st>>>(stats, K, D, (const double *)at(ws, L.cshift), w, mu, sg,
+                              (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0, floor_abs, floor_rel, prior_floor, w_new, mu_new,
+                              var_new);
+  g_launches += 1;
+  return cuda_check("k_mstep");
+}
+
+fv_status check_floors(float floor_abs, float floor_rel, float prior_floor) {
+  if (!(floor_abs >= 0.f) || !(floor_rel >= 0.f) || !(prior_floor >= 0.f) || !(prior_floor < 1.f) ||
+      !std::isfinite(floor_abs) || !std::isfinite(floor_rel))
+    return fail(FV_ERR_ARG, "floors must be finite, >= 0 (prior_floor < 1)");
+  return FV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fv_status fv_gmm_estep(const float *X, int64_t N, int D, const float *w, const float *mu, const float *sg, int K,
+                       unsigned flags, double *stats, double *loglik, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_common(X, N, 1, D, K, 0.f, w, mu, sg, flags)) return s;
+  if (!stats || !loglik) return fail(FV_ERR_ARG, "null stats/loglik");
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(N, 1, K, D, false, L, 0, true)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  return estep_impl(L, X, N, D, w, mu, sg, K, flags, stats, loglik, ws, (cudaStream_t)stream);
+}
+
+fv_status fv_gmm_mstep(const double *stats, int D, const float *w, const float *mu, const float *sg, int K,
+                       unsigned flags, float var_floor_abs, float var_floor_rel, float prior_floor, float *w_new,
+                       float *mu_new, float *var_new, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags)) return s;
+  if (!stats || !w_new || !mu_new || !var_new) return fail(FV_ERR_ARG, "null stats/output");
+  if (fv_status s = check_floors(var_floor_abs, var_floor_rel, prior_floor)) return s;
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(0, 1, K, D, false, L, 0, true)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  return mstep_impl(L, stats, D, w, mu, sg, K, flags, var_floor_abs, var_floor_rel, prior_floor, w_new, mu_new,
+                    var_new, ws, (cudaStream_t)stream);
+}
+
+fv_status fv_gmm_em_step(const float *X, int64_t N, int D, const float *w, const float *mu, const float *sg, int K,
+                         unsigned flags, float var_floor_abs, float var_floor_rel, float prior_floor, float *w_new,
+                         float *mu_new, float *var_new, double *loglik, void *ws, size_t ws_bytes,
+                         fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_common(X, N, 1, D, K, 0.f, w, mu, sg, flags)) return s;
+  if (!w_new || !mu_new || !var_new || !loglik) return fail(FV_ERR_ARG, "null output");
+  if (N < 1) return fail(FV_ERR_ARG, "EM needs N >= 1 descriptors");
+  if (fv_status s = check_floors(var_floor_abs, var_floor_rel, prior_floor)) return s;
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(N, 1, K, D, false, L, 0, true)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  double *stats = (double *)at(ws, L.emstats);
+  if (fv_status s = estep_impl(L, X, N, D, w, mu, sg, K, flags, stats, loglik, ws, st)) return s;
+  return mstep_impl(L, stats, D, w, mu, sg, K, flags | FV_PREPARED, var_floor_abs, var_floor_rel, prior_floor, w_new,
+                    mu_new, var_new, ws, st);
 }
 
 int fv_last_launch_count(void) { return g_launches; }

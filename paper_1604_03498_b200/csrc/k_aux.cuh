@@ -25,7 +25,7 @@ __device__ __forceinline__ double gmm_var(const float *sigmas, size_t i, bool st
 // in log2 units.  One block of 256 threads.
 __global__ void k_prep_shift(const float *w, const float *mu, const float *sg, int K, int D, int Kp,
                              int stddev, double *cshift, float *xshift, float *xscale, float *bias,
-                             double *bscratch) {
+                             double *bscratch, double *bmax_out) {
   __shared__ double s_c[kDMax];
   __shared__ double s_red[256];
   const int tid = threadIdx.x;
@@ -71,6 +71,7 @@ __global__ void k_prep_shift(const float *w, const float *mu, const float *sg, i
     __syncthreads();
   }
   bmax = s_red[0];
+  if (tid == 0) *bmax_out = bmax;  // the bias shift (natural log units): log-likelihoods add it back
   for (int j = tid; j < Kp; j += 256)
     bias[j] = (j < K) ? (float)((bscratch[j] - bmax) * kLog2e) : -1.0e30f;
 }
@@ -518,6 +519,90 @@ __global__ void __launch_bounds__(256) k_reduce_stats(const FinParams p) {
       st[1 + p.K + (size_t)j * p.D + k] = S1[i];
       st[1 + p.K + (size_t)KD + (size_t)j * p.D + k] = S2[i];
     }
+  }
+}
+
+// ---------------------------------------------------------------- GMM EM (NEXT-3)
+// Total log-likelihood of the E-step's descriptors under the input GMM (natural log):
+//   LL = sum_i [ ln2 * ll2_i ] + N (bmax - D/2 ln 2 pi),
+// ll2_i = log2 sum_j 2^(L_ij + b_j) from k_stats (b_j shifted by bmax and missing the -D/2 ln 2pi
+// constant, which cancel in the posteriors, reading A2).  Fixed chunks per block summed in fp64 into
+// the block's slot; the last block (ticket) sums the slots in block order: bitwise repeatable.
+constexpr int kLLBlocks = 296;
+__global__ void __launch_bounds__(256) k_loglik_reduce(const float *ll2, int64_t n, int D, const double *bmax,
+                                                       double *parts, unsigned *ticket, double *out) {
+  __shared__ double s_red[8];
+  __shared__ int s_last;
+  const int tid = threadIdx.x;
+  const int64_t lo = (int64_t)blockIdx.x * n / gridDim.x, hi = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
+  double acc = 0.0;
+  for (int64_t i = lo + tid; i < hi; i += 256) acc += (double)ll2[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((tid & 31) == 0) s_red[tid >> 5] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += s_red[w];
+    parts[blockIdx.x] = t;
+    __threadfence();
+    s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last || tid != 0) return;
+  __threadfence();
+  double t = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(parts + b);
+  const double kLn2 = 0.69314718055994530941723212145818, kLn2Pi = 1.8378770664093454835606594728112;
+  *out = kLn2 * t + (double)n * (*bmax - 0.5 * (double)D * kLn2Pi);
+}
+
+// M-step from the E-step statistics [N, S0 (K), S1 (KxD), S2 (KxD)] about c (reading A19):
+//   mu_j = c + S1_j / S0_j,  var_j = S2_j / S0_j - (S1_j / S0_j)^2  (fp64; the moment form of the
+//   oracle's two-pass definition), var <- max(var, max(floor_abs, floor_rel * var_k(X))) with
+//   var_k(X) = sum_j S2_jk / N - (sum_j S1_jk / N)^2 (exact mode: sum_j gamma_ij = 1),
+//   pi_j = max(S0_j / N, prior_floor) / sum;  S0_j == 0 keeps mu_j and var_j (reading A20).
+// One block of 1024 threads (K(2D+1) <= 131,584 values).
+__global__ void __launch_bounds__(1024) k_mstep(const double *st, int K, int D, const double *cshift, const float *w_old,
+                                                const float *mu_old, const float *sg_old, int stddev, double floor_abs,
+                                                double floor_rel, double prior_floor, float *w_new, float *mu_new,
+                                                float *var_new) {
+  __shared__ double s_floor[kDMax];
+  __shared__ double s_red[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double N = st[0];
+  const double *S0 = st + 1, *S1 = st + 1 + K, *S2 = st + 1 + K + (size_t)K * D;
+  (void)w_old;
+  if (tid < D) {
+    double a = 0.0, b = 0.0;
+    for (int j = 0; j < K; ++j) { a += S1[(size_t)j * D + tid]; b += S2[(size_t)j * D + tid]; }
+    const double m1 = N > 0.0 ? a / N : 0.0;
+    const double gv = N > 0.0 ? b / N - m1 * m1 : 0.0;
+    s_floor[tid] = fmax(floor_abs, floor_rel * gv);
+  }
+  double ps = 0.0;
+  for (int j = tid; j < K; j += 1024) ps += fmax(N > 0.0 ? S0[j] / N : 0.0, prior_floor);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+  if (lane == 0) s_red[wid] = ps;
+  __syncthreads();
+  double tot = 0.0;
+  for (int w = 0; w < 32; ++w) tot += s_red[w];  // fixed order
+  for (int j = tid; j < K; j += 1024) w_new[j] = (float)(fmax(N > 0.0 ? S0[j] / N : 0.0, prior_floor) / tot);
+  for (int e = tid; e < K * D; e += 1024) {
+    const int j = e / D, k = e - j * D;
+    const double s0 = S0[j];
+    double mu, var;
+    if (s0 > 0.0) {
+      const double m1 = S1[e] / s0;
+      mu = cshift[k] + m1;
+      var = S2[e] / s0 - m1 * m1;
+    } else {
+      mu = (double)mu_old[e];
+      var = gmm_var(sg_old, e, stddev != 0);
+    }
+    mu_new[e] = (float)mu;
+    var_new[e] = (float)fmax(var, s_floor[k]);
   }
 }
 

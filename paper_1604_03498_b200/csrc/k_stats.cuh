@@ -86,6 +86,7 @@ struct Stats2Params {
   float *slots;               // segment slots: (ncl + batch) x kNF x Kp   (feature-major rows)
   float *s0slots;             // (ncl + batch) x Kp
   float *gamma_out;
+  float *loglik_out;          // n_total (optional): per-descriptor log2 sum_j 2^(L_ij + b_j) (EM E-step)
   long long *trace;           // debug (GPUFV_TRACE builds): per-tile phase clocks of CTA 0
   int batch, D, K, Kp;
   float threshold;
@@ -506,6 +507,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
 #pragma unroll
         for (int e = 0; e < kMaxC2 * 4; ++e) S += o[e].y * ex2_approx(o[e].x - M);
       }
+      // per-descriptor log2-likelihood (EM, NEXT-3): log2 sum_j 2^(L_ij + b_j) = M + log2 S
+      if (p.loglik_out && h == 0 && rank == 0 && row < mt.nrows) p.loglik_out[mt.row0 + row] = M + log2f(S);
       // this quarter's gamma_ij = e_ij 2^(m_h - M) / S; P = gamma 2^14
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
       if (row >= mt.nrows) alpha_p = 0.f;

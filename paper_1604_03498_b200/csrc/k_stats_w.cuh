@@ -355,6 +355,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         M = Mg;
         S = Sg;
       }
+      // per-descriptor log2-likelihood (EM, NEXT-3)
+      if (p.loglik_out && h == 0 && rank == 0 && row < mt.nrows) p.loglik_out[mt.row0 + row] = M + log2f(S);
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
       if (row >= mt.nrows) alpha_p = 0.f;
       TRW(4);

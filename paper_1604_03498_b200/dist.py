@@ -102,3 +102,34 @@ def encode_descriptor_sharded(X_shard, gmm, threshold: float = 0.0, mode: int = 
         else:
             dist.all_reduce(st, op=dist.ReduceOp.SUM, group=group)  # a8
     return finalize_fn(st).reshape(-1)
+
+
+def em_step_sharded(X_shard, gmm, group=None, estep_fn=None, mstep_fn=None, deterministic: bool = False,
+                    **floors):
+    """One EM iteration (NEXT-3) over a descriptor set sharded by rows across ranks: every rank runs the
+    E-step on its shard (sufficient statistics [N, S0, S1, S2] about c and the log-likelihood sum), the
+    1 + K(2D+1) + 1 fp64 values are summed with one all_reduce (they add across shards, reading A19),
+    and every rank runs the same M-step.  Returns (new GMM, total log-likelihood under the input GMM)."""
+    rank, world = _rank_world(group)
+    if estep_fn is None:
+        from . import gmm_estep as _estep
+
+        def estep_fn(Xs):
+            return _estep(Xs, gmm)
+    if mstep_fn is None:
+        from . import gmm_mstep as _mstep
+
+        def mstep_fn(st):
+            return _mstep(st, gmm, **floors)
+    st, ll = estep_fn(X_shard)
+    buf = torch.cat([st.reshape(-1).to(torch.float64), ll.reshape(-1).to(torch.float64)])
+    if world > 1:
+        if deterministic:
+            parts = [torch.empty_like(buf) for _ in range(world)]
+            dist.all_gather(parts, buf, group=group)
+            buf = parts[0].clone()
+            for t in parts[1:]:
+                buf += t  # fixed rank order
+        else:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return mstep_fn(buf[:-1].contiguous()), float(buf[-1].item())

@@ -36,5 +36,32 @@ out = fvd.encode_frames_sharded(
     Xb, off, gmm, encode_fn=lambda Xs, o: torch.from_numpy(oracle.encode_batched(Xs, o.numpy(), *gmm, threshold=1e-6)),
     gather=True)
 res["frames"] = out.numpy()
+
+
+def mstep_from_stats(st):
+    """Test-local M-step in the statistics' moment form (about c), to compare against the oracle's
+    two-pass em_step on the whole set."""
+    pi, mu, var = (a.astype(np.float64) for a in gmm)
+    K, D = mu.shape
+    st = st.numpy()
+    N, S0 = st[0], st[1:1 + K]
+    S1 = st[1 + K:1 + K + K * D].reshape(K, D)
+    S2 = st[1 + K + K * D:].reshape(K, D)
+    c = (pi[:, None] * mu).sum(0) / pi.sum()
+    m1 = S1 / S0[:, None]
+    gvar = S2.sum(0) / N - (S1.sum(0) / N) ** 2
+    v = np.maximum(S2 / S0[:, None] - m1 ** 2, np.maximum(1e-6, 1e-4 * gvar)[None])
+    w = np.maximum(S0 / N, 1e-8)
+    return w / w.sum(), c + m1, v
+
+
+for det in (False, True):
+    new, ll = fvd.em_step_sharded(
+        X[lo:hi], gmm,
+        estep_fn=lambda Xs: (torch.from_numpy(oracle.stats(Xs, *gmm)),
+                             torch.tensor([oracle.loglik_rows(Xs, *gmm).sum()], dtype=torch.float64)),
+        mstep_fn=mstep_from_stats, deterministic=det)
+    res[f"em_pi_{det}"], res[f"em_mu_{det}"], res[f"em_var_{det}"] = new
+    res[f"em_ll_{det}"] = np.array([ll])
 np.savez(os.path.join(os.environ["OUT_DIR"], f"rank{rank}.npz"), **res)
 dist.destroy_process_group()

@@ -73,3 +73,17 @@ def test_partitions():
     assert sorted(sum(parts, [])) == list(range(7))
     loads = [sum(counts[i] for i in p) for p in parts]
     assert max(loads) <= 100
+
+
+def test_em_sharded_allreduce_equals_whole_set_em(results):
+    """Sharded E-step statistics + log-likelihood summed over 2 ranks, then the moment-form M-step,
+    equals the oracle's two-pass EM step on the whole set (NEXT-3)."""
+    gmm = fvgen.make_gmm(16, 8, seed=31)
+    X = fvgen.make_descriptors(gmm, 2001, seed=32)
+    pi, mu, var, ll = oracle.em_step(X, *gmm)
+    for r in (0, 1):
+        for det in (False, True):
+            np.testing.assert_allclose(results[r][f"em_pi_{det}"], pi, rtol=1e-10)
+            np.testing.assert_allclose(results[r][f"em_mu_{det}"], mu, rtol=1e-9, atol=1e-12)
+            np.testing.assert_allclose(results[r][f"em_var_{det}"], var, rtol=1e-8)
+            assert results[r][f"em_ll_{det}"][0] == pytest.approx(ll, rel=1e-12)
