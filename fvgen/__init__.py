@@ -117,3 +117,49 @@ CONFIGS = {
     "C4": dict(K=256, D=64, frames=4096, per_frame=5000, seed_gmm=1604, seed_data=1604 + 20000),
     "C5": dict(K=512, D=128, counts=[10_000_000], seed_gmm=1605, seed_data=1605 + 1),
 }
+
+
+# ---------------------------------------------------------------- raw SIFT-shaped inputs (NEXT-2)
+SIFT_DIM = 128
+
+
+def make_pca(m: int, seed: int = 1604 + 50, in_dim: int = SIFT_DIM):
+    """A PCA model (SPEC embed.PcaModel): mean (in_dim,) nonnegative SIFT-like, basis (m, in_dim) with
+    orthonormal rows (QR of a seeded Gaussian matrix, sign-fixed).  float32."""
+    rng = np.random.default_rng(seed)
+    mean = np.abs(rng.normal(0.05, 0.03, in_dim))
+    q, r = np.linalg.qr(rng.standard_normal((in_dim, m)))
+    q = q * np.sign(np.diag(r))[None, :]
+    return mean.astype(np.float32), np.ascontiguousarray(q.T).astype(np.float32)
+
+
+def make_embedded_gmm(K: int, m: int, seed: int = SEED_GMM):
+    """GMM over the embedded M = m + 2 dims: the first m from the acceptance recipe (make_gmm), the last
+    two (normalised x, y in [0, 1]) with means U(0.2, 0.8) and std-devs U(0.15, 0.3)."""
+    pi, mu, var = make_gmm(K, m, seed=seed)
+    rng = np.random.default_rng(seed + 7)
+    mxy = rng.uniform(0.2, 0.8, (K, 2))
+    sxy = rng.uniform(0.15, 0.3, (K, 2))
+    return (pi, np.concatenate([mu, mxy.astype(np.float32)], 1),
+            np.concatenate([var, (sxy * sxy).astype(np.float32)], 1))
+
+
+def make_raw_frames(gmm_m, pca, counts, seed: int, img_wh=(320, 240), resid: float = 0.01):
+    """Raw 128-d descriptors whose PCA projection follows the m-dim GMM `gmm_m` (first m dims of an
+    embedded GMM): raw = mean + basis^T y + resid * (noise orthogonal to the basis); keypoints uniform
+    over a img_wh image.  Returns (raw (N, 128), xy (N, 2) pixels, offsets (B+1,), wh (B, 2)), float32."""
+    mean, basis = pca
+    m = basis.shape[0]
+    pi, mu, var = gmm_m
+    mu, var = mu[:, :m], var[:, :m]
+    counts = np.asarray(counts, dtype=np.int64)
+    off = np.zeros(len(counts) + 1, dtype=np.int64)
+    off[1:] = np.cumsum(counts)
+    Y = make_frames((pi, mu, var), 1, int(off[-1]), seed=seed) if off[-1] > 0 else np.zeros((0, m), np.float32)
+    rng = np.random.default_rng(seed + 1)
+    E = rng.standard_normal((Y.shape[0], basis.shape[1])).astype(np.float32)
+    E -= (E @ basis.T) @ basis
+    raw = (mean[None, :] + Y @ basis + resid * E).astype(np.float32)
+    wh = np.tile(np.asarray(img_wh, np.float32), (len(counts), 1))
+    xy = (rng.random((Y.shape[0], 2)) * np.repeat(wh, counts, axis=0)).astype(np.float32)
+    return raw, xy, off, wh

@@ -14,6 +14,7 @@ from .oracle import (  # noqa: F401
     NORM_POWER_L2,
     accumulate,
     build,
+    embed,
     em_step,
     encode,
     encode_batched,

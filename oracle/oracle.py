@@ -247,3 +247,17 @@ def em_step(X, priors, means, variances, var_floor_abs: float = 1e-6, var_floor_
     pi = np.maximum(Nj / N, prior_floor)
     pi = pi / pi.sum()
     return pi, mu, var, LL
+
+
+# ------------------------------------------------------------------ PCA + xy embedding (NEXT-2)
+def embed(raw, xy, offsets, wh, pca_mean, pca_basis) -> np.ndarray:
+    """P:138 [§3.1]: "by lowering the dimension to m (m<128) with PCA and adding the normalized X and Y
+    axis, a descriptor with dimension M=m+2 is generated" (SPEC embed S:201-203):
+      row_i = [ basis (d_i - mean) ; x_i / W_b ; y_i / H_b ]   for descriptor i of image b,
+    basis (m, 128), no whitening.  float64, (N, m + 2)."""
+    raw, xy, wh = _d(raw), _d(xy), _d(wh)
+    mean, B = _d(pca_mean), _d(pca_basis)
+    off = np.asarray(offsets, dtype=np.int64)
+    img = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    proj = (raw - mean[None, :]) @ B.T
+    return np.concatenate([proj, xy / wh[img]], axis=1)

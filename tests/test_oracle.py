@@ -424,3 +424,44 @@ def test_em_floors_and_component_permutation():
     np.testing.assert_allclose(pp, pi[perm], rtol=1e-12)
     np.testing.assert_allclose(mp_, mu[perm], rtol=1e-12)
     np.testing.assert_allclose(vp, var[perm], rtol=1e-12)
+
+
+# ---------------------------------------------------------------- PCA + xy embedding (NEXT-2)
+def test_embed_closed_forms():
+    """SPEC embed examples: d = mean -> first m coords zero; keypoint at the image centre -> (0.5, 0.5);
+    a full orthonormal basis (m = 128) preserves ||d - mean|| (closed form); basis rows = unit vectors
+    pick coordinates of d - mean; the two images use their own sizes."""
+    mean, B = fvgen.make_pca(80, seed=3)
+    raw = np.stack([mean, mean + 1.0]).astype(np.float32)
+    xy = np.array([[160.0, 120.0], [50.0, 100.0]], np.float32)
+    off = np.array([0, 1, 2])
+    wh = np.array([[320.0, 240.0], [100.0, 400.0]], np.float32)
+    E = oracle.embed(raw, xy, off, wh, mean, B)
+    assert E.shape == (2, 82)
+    np.testing.assert_allclose(E[0, :80], 0.0, atol=1e-12)
+    np.testing.assert_allclose(E[0, 80:], [0.5, 0.5]); np.testing.assert_allclose(E[1, 80:], [0.5, 0.25])
+    mf, Bf = fvgen.make_pca(128, seed=4)
+    d = np.random.default_rng(5).normal(size=(7, 128))
+    Ef = oracle.embed(d, np.zeros((7, 2)), [0, 7], [[1.0, 1.0]], mf, Bf)
+    np.testing.assert_allclose(np.linalg.norm(Ef[:, :128], axis=1), np.linalg.norm(d - mf, axis=1), rtol=1e-6)
+    I = np.eye(128)[[3, 0, 127]]
+    Ei = oracle.embed(d, np.zeros((7, 2)), [0, 7], [[1.0, 1.0]], np.zeros(128), I)
+    np.testing.assert_array_equal(Ei[:, :3], d[:, [3, 0, 127]])
+
+
+def test_embed_is_linear_and_generator_is_consistent():
+    """Projection is linear (SPEC invariant); the raw generator's descriptors project back to the
+    m-dim GMM sample up to the small orthogonal residual."""
+    mean, B = fvgen.make_pca(80, seed=6)
+    rng = np.random.default_rng(7)
+    d1, d2 = rng.normal(size=(2, 5, 128))
+    z = np.zeros((5, 2))
+    a = 0.3
+    np.testing.assert_allclose(oracle.embed(a * d1 + (1 - a) * d2, z, [0, 5], [[1, 1]], mean, B)[:, :80],
+                               a * oracle.embed(d1, z, [0, 5], [[1, 1]], mean, B)[:, :80]
+                               + (1 - a) * oracle.embed(d2, z, [0, 5], [[1, 1]], mean, B)[:, :80], atol=1e-12)
+    gmm = fvgen.make_embedded_gmm(8, 80, seed=8)
+    raw, xy, off, wh = fvgen.make_raw_frames(gmm, (mean, B), [300, 200], seed=9)
+    E = oracle.embed(raw, xy, off, wh, mean, B)
+    assert E.shape == (500, 82) and np.all((E[:, 80:] >= 0) & (E[:, 80:] <= 1))
+    assert np.abs(E[:, :80]).max() < 5.0
