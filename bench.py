@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--score-steps", type=int, default=5,
                     help="steps of the fused-scoring monitoring leg (NEXT-4; 0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="wall budget of the oracle sample")
-    ap.add_argument("--workload", default="c4", choices=["c4", "c5", "em"],
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5", "em", "embed"],
                     help="c4: frame-sharded stream (default, the metric's config); c5: one 10M x 128 set, K=512, "
                          "descriptor-sharded with an NCCL all-reduce of the fp64 statistics")
     ap.add_argument("--c5-n", type=int, default=10_000_000, help="C5 set size (all ranks together)")
@@ -491,6 +491,109 @@ def run_em(args, rank, world, local):
         torch.distributed.destroy_process_group()
 
 
+def run_embed(args, rank, world, local):
+    """Raw dense-SIFT-shaped descriptors -> FVs: a 320x240-frame
+    stream (min(frames, 1024) frames x 5000 raw 128-d descriptors + keypoints per rank), PCA to m = 80
+    plus normalised xy (D = 82, the paper's format), K = 256, tau = 1e-6; one step = fv_embed_encode_batched
+    (k_embed + the encode path).  The embedding kernel is also timed alone (fp32 FMA bound)."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1604_03498_b200 as fv
+    m, Ke = 80, 256
+    frames = min(args.frames, 1024)
+    pca = fvgen.make_pca(m, seed=1604 + 50)
+    gmm_np = fvgen.make_embedded_gmm(Ke, m, seed=1604)
+    raw, xy, off, wh = fvgen.make_raw_frames(gmm_np, pca, [PER_FRAME] * frames, seed=1604 + 40000 + rank * 1_000_003)
+    n = raw.shape[0]
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    rawd, xyd, offd, whd, meand, Bd = t(raw), t(xy), t(off), t(wh), t(pca[0]), t(pca[1])
+    gmm = fv.GMM(*gmm_np, device=dev)
+    ws = fv.Workspace(device=dev)
+    ws.ensure(int(fv.lib.fv_workspace_bytes_embed(n, frames, Ke, m, 0)))
+    out = torch.empty(frames, 2 * Ke * (m + 2), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        fv.embed_encode_batched(rawd, xyd, offd, whd, meand, Bd, gmm, threshold=TAU, ws=ws, out=out)
+
+    step()
+    torch.cuda.synchronize(dev)
+    parity = None
+    if rank == 0:
+        import oracle
+        res = out.cpu().numpy()
+        errs = []
+        for f in (0, frames - 1):
+            sl = slice(f * PER_FRAME, (f + 1) * PER_FRAME)
+            E = oracle.embed(raw[sl], xy[sl], [0, PER_FRAME], wh[f:f + 1], *pca)
+            ref = oracle.encode(E, *gmm_np, threshold=TAU)
+            errs.append(float(np.linalg.norm(res[f] - ref) / np.linalg.norm(ref)))
+        parity = {"frames_checked": 2, "max_rel_l2": max(errs), "tolerance": 1e-4}
+        if max(errs) > 1e-4:
+            raise SystemExit(f"parity failure before timing: {errs}")
+    clk = ClockSampler(local, pci_bus_id(dev)).__enter__()
+    for _ in range(max(3, args.warmup)):
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clk.mark_start()
+    try:
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    finally:
+        clk.mark_stop()
+        clk.__exit__(None, None, None)
+    total_ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms = total_ms / args.steps
+    # the embedding kernel alone
+    Xe = torch.empty(n, 84, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        fv.lib.fv_embed(fv._ptr(rawd), fv._ptr(xyd), fv._ptr(offd), frames, n, fv._ptr(whd), fv._ptr(meand),
+                        fv._ptr(Bd), m, fv._ptr(Xe), 84, fv._stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        fv.lib.fv_embed(fv._ptr(rawd), fv._ptr(xyd), fv._ptr(offd), frames, n, fv._ptr(whd), fv._ptr(meand),
+                        fv._ptr(Bd), m, fv._ptr(Xe), 84, fv._stream())
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ems = e0.elapsed_time(e1) / args.steps
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    fma_peak = 148 * 128 * 2 * 1.965e-3  # TFLOP/s: SMs x fp32 FMA lanes x 2 x max SM clock (1.965 GHz)
+    emb_tf = 2.0 * 128 * m * n / (ems * 1e-3) / 1e12
+    line = {
+        "metric": f"descriptors/sec raw SIFT -> FV (PCA m={m} + xy, D={m + 2}, K={Ke})",
+        "value": world * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 embed + f16 split encode", "data": "synthetic",
+        "config": {"workload": f"{frames} frames x {PER_FRAME} raw 128-d descriptors per rank, m={m}, D={m + 2}, "
+                               f"K={Ke}, tau={TAU}", "parallelism": f"frame-sharded x{world}"},
+        "embed_kernel": {"ms": ems, "share_of_step": ems / ms, "roofline": {
+            "bound": "alu", "achieved": emb_tf, "peak": fma_peak, "unit": "TFLOP/s", "frac": emb_tf / fma_peak,
+            "peak_source": "148 SMs x 128 fp32 FMA/clk x 2 FLOP x 1.965 GHz (B200_PROFILING.md unit counts, max clock)"}},
+        "clocks": clk.summary(), "parity": parity, "gpu_launches": None, "e2e": None, "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -502,6 +605,9 @@ def main():
         return
     if args.workload == "em":
         run_em(args, rank, world, local)
+        return
+    if args.workload == "embed":
+        run_embed(args, rank, world, local)
         return
     import torch
     torch.cuda.set_device(local)

@@ -176,6 +176,30 @@ fv_status fv_gmm_em_step(const float *X, int64_t N, int D, const float *weights,
                          float prior_floor, float *new_weights, float *new_means, float *new_vars, double *loglik,
                          void *ws, size_t ws_bytes, fv_stream_t stream);
 
+/* PCA + normalised-xy embedding, the step upstream of the encoder ("by lowering
+ * the dimension to m (m<128) with PCA and adding the normalized X and Y axis, a descriptor with
+ * dimension M=m+2 is generated", §3.1; SPEC embed S:201-203; no whitening):
+ *   X_out[i * ldx + c] = sum_k pca_basis[c * 128 + k] (raw[i * 128 + k] - pca_mean[k])   (c < m)
+ *   X_out[i * ldx + m] = xy[2 i] / img_wh[2 b],  X_out[i * ldx + m + 1] = xy[2 i + 1] / img_wh[2 b + 1]
+ *   X_out[i * ldx + c] = 0 for m + 2 <= c < ldx,
+ * for descriptor i of image b (rows offsets[b] .. offsets[b+1]-1).  raw: device, n_total x 128 fp32
+ * (16-byte aligned); xy: n_total x 2 keypoint pixel coordinates in the original image; img_wh: batch x
+ * 2 (width, height); pca_mean: 128; pca_basis: m x 128 row-major (rows orthonormal: not checked);
+ * 1 <= m <= 126; ldx >= m + 2, ldx % 4 == 0.  fp32 accumulation in k = 0..127 order. */
+fv_status fv_embed(const float *raw, const float *xy, const int64_t *offsets, int batch, int64_t n_total,
+                   const float *img_wh, const float *pca_mean, const float *pca_basis, int m, float *X_out, int ldx,
+                   fv_stream_t stream);
+
+/* Raw descriptors to FVs in one call: fv_embed into the workspace (row stride round_up(m+2, 4)), then
+ * the fv_encode_batched path with D = m + 2 (any D: the stride padding makes the rows TMA-aligned).
+ * The GMM is K x (m + 2).  out: batch x 2K(m+2).  ws >= fv_workspace_bytes_embed(n_total, batch, K, m, flags). */
+size_t fv_workspace_bytes_embed(int64_t n_total, int batch, int K, int m, unsigned flags);
+fv_status fv_embed_encode_batched(const float *raw, const float *xy, const int64_t *offsets, int batch,
+                                  int64_t n_total, const float *img_wh, const float *pca_mean,
+                                  const float *pca_basis, int m, const float *weights, const float *means,
+                                  const float *sigmas, int K, float threshold, unsigned flags, float *out,
+                                  void *ws, size_t ws_bytes, fv_stream_t stream);
+
 /* Test hook: posteriors gamma (N x K fp32) of one set, computed by the production kernel (same
  * GEMM + softmax path as fv_encode); entries <= threshold are zeroed when threshold > 0. */
 fv_status fv_posteriors(const float *X, int64_t N, int D, const float *weights, const float *means,

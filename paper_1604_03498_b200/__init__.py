@@ -17,7 +17,7 @@ __all__ = [
     "GMM", "Workspace", "lib", "lib_path", "workspace_bytes", "gmm_prepare", "encode", "encode_batched",
     "encode_batched_host", "stats_batched", "finalize", "posteriors", "last_launch_count", "profile_events",
     "encode_scored_batched", "encode_scored_batched_host", "MAX_CLASSES", "gmm_estep", "gmm_mstep", "gmm_em_step",
-    "gmm_fit", "FVError",
+    "gmm_fit", "embed", "embed_encode_batched", "FVError",
 ]
 
 NORM_IMPROVED = 0
@@ -65,7 +65,12 @@ lib.fv_gmm_estep.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _u32, _vp, _v
 lib.fv_gmm_mstep.argtypes = [_vp, _i32, _vp, _vp, _vp, _i32, _u32, _f32, _f32, _f32, _vp, _vp, _vp, _vp, _sz, _vp]
 lib.fv_gmm_em_step.argtypes = [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _u32, _f32, _f32, _f32, _vp, _vp, _vp, _vp, _vp,
                                _sz, _vp]
-for _fn in ("fv_gmm_estep", "fv_gmm_mstep", "fv_gmm_em_step"):
+lib.fv_embed.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _vp, _i32, _vp]
+lib.fv_workspace_bytes_embed.argtypes = [_i64, _i32, _i32, _i32, _u32]
+lib.fv_workspace_bytes_embed.restype = _sz
+lib.fv_embed_encode_batched.argtypes = [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _f32, _u32,
+                                        _vp, _vp, _sz, _vp]
+for _fn in ("fv_gmm_estep", "fv_gmm_mstep", "fv_gmm_em_step", "fv_embed", "fv_embed_encode_batched"):
     getattr(lib, _fn).restype = _i32
 for _fn in ("fv_gmm_prepare", "fv_encode", "fv_encode_batched", "fv_encode_batched_host", "fv_stats_batched",
             "fv_finalize", "fv_posteriors", "fv_encode_scored_batched", "fv_encode_scored_batched_host"):
@@ -400,3 +405,46 @@ def gmm_fit(X, init: GMM, max_iters: int = 100, tol: float = 1e-6, **floors):
         if len(hist) > 1 and abs(hist[-1] - hist[-2]) <= tol * abs(hist[-2]):
             break
     return cur, hist
+
+
+# ------------------------------------------------------------------ PCA + xy embedding (NEXT-2)
+def _check_embed_inputs(raw, xy, offsets, img_wh, pca_mean, pca_basis):
+    for name, t, cols in (("raw", raw, 128), ("xy", xy, 2), ("img_wh", img_wh, 2)):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.dim() == 2 and t.shape[1] == cols):
+            raise ValueError(f"{name} must be a contiguous float32 CUDA tensor (*, {cols})")
+    if not (offsets.is_cuda and offsets.dtype == torch.int64):
+        raise ValueError("offsets must be an int64 CUDA tensor")
+    if not (pca_basis.is_cuda and pca_basis.dtype == torch.float32 and pca_basis.is_contiguous()
+            and pca_basis.shape[1] == 128 and pca_mean.numel() == 128):
+        raise ValueError("pca_mean (128,) and pca_basis (m, 128) must be contiguous float32 CUDA tensors")
+    return pca_basis.shape[0]
+
+
+def embed(raw, xy, offsets, img_wh, pca_mean, pca_basis, ldx: int | None = None):
+    """Raw SIFT (N, 128) + keypoints (N, 2) -> (N, ldx) float32 = [PCA (m), x/W, y/H, 0 pad]."""
+    m = _check_embed_inputs(raw, xy, offsets, img_wh, pca_mean, pca_basis)
+    ldx = ldx or (m + 2 + 3) // 4 * 4
+    out = torch.empty(raw.shape[0], ldx, dtype=torch.float32, device=raw.device)
+    _check(lib.fv_embed(_ptr(raw), _ptr(xy), _ptr(offsets), offsets.shape[0] - 1, raw.shape[0], _ptr(img_wh),
+                        _ptr(pca_mean), _ptr(pca_basis), m, _ptr(out), ldx, _stream()))
+    return out
+
+
+def embed_encode_batched(raw, xy, offsets, img_wh, pca_mean, pca_basis, gmm: GMM, threshold: float = 0.0,
+                         mode: int = NORM_IMPROVED, ws: Workspace | None = None, out=None):
+    """Raw descriptors -> FVs (batch, 2K(m+2)) in one call; gmm is K x (m+2)."""
+    m = _check_embed_inputs(raw, xy, offsets, img_wh, pca_mean, pca_basis)
+    if gmm.D != m + 2:
+        raise ValueError(f"GMM dimension {gmm.D} != m + 2 = {m + 2}")
+    B = offsets.shape[0] - 1
+    need = int(lib.fv_workspace_bytes_embed(raw.shape[0], B, gmm.K, m, 0))
+    if need == 0:
+        raise FVError(1)
+    ws, _ = _ws(ws, need, raw.device)
+    if out is None:
+        out = torch.empty(B, 2 * gmm.K * gmm.D, dtype=torch.float32, device=raw.device)
+    w, mu, s = gmm.ptrs()
+    _check(lib.fv_embed_encode_batched(_ptr(raw), _ptr(xy), _ptr(offsets), B, raw.shape[0], _ptr(img_wh),
+                                       _ptr(pca_mean), _ptr(pca_basis), m, w, mu, s, gmm.K, float(threshold),
+                                       _mode_flags(gmm, mode, False), _ptr(out), *ws.args(), _stream()))
+    return out

@@ -18,6 +18,7 @@
 #include "k_aux.cuh"
 #include "k_stats.cuh"
 #include "k_stats_w.cuh"
+#include "k_embed.cuh"
 
 using namespace gpufv;
 
@@ -98,11 +99,13 @@ struct Layout {
   size_t tiles, off1, cstart, cown, norm2, s0slots, slots;  // per call
   size_t spart;                                           // fused scoring partial dots (n_cls > 0)
   size_t llrows, llparts, emstats;                        // EM: per-row log2-likelihoods, reduction, stats
+  size_t emb;                                             // embedded descriptors (n_total x ldx), NEXT-2
   size_t hx, hoff, hout;                                  // _host entry point
   size_t total;
 };
 
-bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout &L, int n_cls = 0, bool em = false) {
+bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout &L, int n_cls = 0, bool em = false,
+                 int emb_ld = 0) {
   L.C = cluster_size(K, D);
   L.Kp = L.C * gauss_per_cta(K, D);
   L.dpad = is_wide(K, D) ? kDMax : kDP;
@@ -138,6 +141,8 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
     L.llparts = o; o = align_up(o + (size_t)kLLBlocks * 8 + 8, 1024);  // block slots + ticket
     L.emstats = o; o = align_up(o + ((size_t)1 + (size_t)K * (2 * D + 1)) * 8, 1024);
   }
+  L.emb = o;
+  if (emb_ld > 0) o = align_up(o + (size_t)n_total * emb_ld * 4, 1024);
   L.hx = L.hoff = L.hout = 0;
   if (host_io) {
     // device staging of X, offsets and the per-image result (scores when n_cls > 0, else FVs)
@@ -149,12 +154,13 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   return true;
 }
 
-fv_status check_gmm_args(int K, int D, const float *w, const float *mu, const float *sg, unsigned flags) {
+fv_status check_gmm_args(int K, int D, const float *w, const float *mu, const float *sg, unsigned flags,
+                         bool need_d4 = true) {
   if (!w || !mu || !sg) return fail(FV_ERR_ARG, "null GMM pointer");
   if (K < 1 || D < 1) return fail(FV_ERR_ARG, "K=%d and D=%d must be >= 1", K, D);
   if (K > kMaxK) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kMaxK);
   if (D > kDMax) return fail(FV_ERR_UNSUPPORTED, "D=%d > %d", D, kDMax);
-  if (D % 4 != 0) return fail(FV_ERR_UNSUPPORTED, "D=%d is not a multiple of 4 (pad, reading A13)", D);
+  if (need_d4 && D % 4 != 0) return fail(FV_ERR_UNSUPPORTED, "D=%d is not a multiple of 4 (pad, reading A13)", D);
   const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED;
   if (flags & ~known) return fail(FV_ERR_ARG, "unknown flag bits 0x%x", flags & ~known);
   if ((flags & FV_NORM_MASK) == 3) return fail(FV_ERR_ARG, "invalid normalisation mode 3");
@@ -198,7 +204,8 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
 // a2-a6 over a batch: schedule + persistent stats kernel.  gamma (optional) for fv_posteriors.
 fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets, int64_t n_single, int batch, int D,
                        int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st,
-                       float *loglik_rows = nullptr) {
+                       float *loglik_rows = nullptr, int ldx = 0) {
+  if (ldx <= 0) ldx = D;
   // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
   int64_t *off1 = (int64_t *)at(ws, L.off1);
   k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles), L.ncl,
@@ -222,6 +229,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.D = D;
   p.K = K;
   p.Kp = L.Kp;
+  p.ldx = ldx;
   p.threshold = thr > 0.f ? thr : 0.f;
   p.gamma_mode = gamma_mode;
   // X as a 2-D tensor map: dims {D, n_total}, boxes of 32 floats x 128 rows, 128B swizzle; rows past
@@ -237,7 +245,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
       encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
     cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(L.n_total > 0 ? L.n_total : 1)};
-    cuuint64_t strides[1] = {(cuuint64_t)D * 4};
+    cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
     cuuint32_t box[2] = {32, 128};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(X), dims, strides, box, estr,
@@ -326,7 +334,7 @@ struct Scoring {
 fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D,
                               const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
                               float *out, void *ws, size_t ws_bytes, cudaStream_t st, const Layout *Lin,
-                              const Scoring &sc = Scoring()) {
+                              const Scoring &sc = Scoring(), int ldx = 0) {
   Layout L;
   if (Lin) L = *Lin;
   else if (!make_layout(n_total, batch, K, D, false, L, sc.n_cls)) return fail(FV_ERR_CUDA, "occupancy query failed");
@@ -334,7 +342,7 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   if (!(flags & FV_PREPARED))
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
   if (batch == 0) return FV_OK;
-  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st)) return s;
+  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx)) return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   f.out = out;
   f.svm_w = sc.w; f.svm_b = sc.b; f.n_cls = sc.n_cls; f.scores = sc.scores;
@@ -707,6 +715,95 @@ fv_status fv_gmm_em_step(const float *X, int64_t N, int D, const float *w, const
   if (fv_status s = estep_impl(L, X, N, D, w, mu, sg, K, flags, stats, loglik, ws, st)) return s;
   return mstep_impl(L, stats, D, w, mu, sg, K, flags | FV_PREPARED, var_floor_abs, var_floor_rel, prior_floor, w_new,
                     mu_new, var_new, ws, st);
+}
+
+}  // extern "C"
+
+namespace {
+
+constexpr int kEmbLd(int m) { return (m + 2 + 3) / 4 * 4; }
+
+fv_status check_embed_args(const float *raw, const float *xy, const int64_t *offsets, int batch, int64_t n_total,
+                           const float *wh, const float *mean, const float *basis, int m) {
+  if (m < 1 || m > kEmbMaxM) return fail(FV_ERR_ARG, "m=%d must be in [1, %d]", m, kEmbMaxM);
+  if (n_total < 0 || batch < 0) return fail(FV_ERR_ARG, "n_total/batch < 0");
+  if (n_total >= ((int64_t)1 << 30)) return fail(FV_ERR_UNSUPPORTED, "n_total >= 2^30 per call");
+  if (!mean || !basis) return fail(FV_ERR_ARG, "null PCA model");
+  if (batch > 0 && (!offsets || !wh)) return fail(FV_ERR_ARG, "null offsets/img_wh");
+  if (n_total > 0 && (!raw || !xy)) return fail(FV_ERR_ARG, "null raw/xy");
+  if ((raw && reinterpret_cast<uintptr_t>(raw) % 16) || reinterpret_cast<uintptr_t>(mean) % 16 ||
+      (xy && reinterpret_cast<uintptr_t>(xy) % 8) || (wh && reinterpret_cast<uintptr_t>(wh) % 8))
+    return fail(FV_ERR_UNSUPPORTED, "raw/mean must be 16-byte and xy/img_wh 8-byte aligned");
+  return FV_OK;
+}
+
+fv_status launch_embed(const float *raw, const float *xy, const int64_t *offsets, int batch, int64_t n_total,
+                       const float *wh, const float *mean, const float *basis, int m, float *out, int ldx,
+                       cudaStream_t st) {
+  if (n_total == 0 || batch == 0) return FV_OK;
+  EmbedParams e;
+  e.raw = raw; e.xy = xy; e.offsets = offsets; e.wh = wh; e.mean = mean; e.basis = basis; e.out = out;
+  e.n = n_total; e.batch = batch; e.m = m; e.mpad = (m + 7) / 8 * 8; e.ldx = ldx;
+  const int smem = (kEmbIn * e.mpad + kEmbRows * kEmbXStride) * 4;
+  if (cudaFuncSetAttribute(k_embed, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return cuda_check("k_embed attribute");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ntiles = (n_total + kEmbRows - 1) / kEmbRows;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * 2);
+  k_embed<<<grid, 256, smem, st>>>(e);
+  g_launches += 1;
+  return cuda_check("k_embed");
+}
+
+}  // namespace
+
+extern "C" {
+
+fv_status fv_embed(const float *raw, const float *xy, const int64_t *offsets, int batch, int64_t n_total,
+                   const float *img_wh, const float *pca_mean, const float *pca_basis, int m, float *X_out, int ldx,
+                   fv_stream_t stream) {
+  g_launches = 0;
+  if (fv_status s = check_embed_args(raw, xy, offsets, batch, n_total, img_wh, pca_mean, pca_basis, m)) return s;
+  if (n_total > 0 && !X_out) return fail(FV_ERR_ARG, "null X_out");
+  if (ldx < m + 2 || ldx % 4) return fail(FV_ERR_ARG, "ldx=%d must be >= m+2 and a multiple of 4", ldx);
+  if (X_out && reinterpret_cast<uintptr_t>(X_out) % 16) return fail(FV_ERR_UNSUPPORTED, "X_out must be 16-byte aligned");
+  if (fv_status s = check_device()) return s;
+  return launch_embed(raw, xy, offsets, batch, n_total, img_wh, pca_mean, pca_basis, m, X_out, ldx,
+                      (cudaStream_t)stream);
+}
+
+size_t fv_workspace_bytes_embed(int64_t n_total, int batch, int K, int m, unsigned flags) {
+  (void)flags;
+  Layout L;
+  if (K < 1 || K > kMaxK || batch < 0 || n_total < 0 || m < 1 || m > kEmbMaxM) return 0;
+  if (!make_layout(n_total, batch, K, m + 2, false, L, 0, false, kEmbLd(m))) return 0;
+  return L.total;
+}
+
+fv_status fv_embed_encode_batched(const float *raw, const float *xy, const int64_t *offsets, int batch,
+                                  int64_t n_total, const float *img_wh, const float *pca_mean,
+                                  const float *pca_basis, int m, const float *w, const float *mu, const float *sg,
+                                  int K, float thr, unsigned flags, float *out, void *ws, size_t ws_bytes,
+                                  fv_stream_t stream) {
+  g_launches = 0;
+  const int D = m + 2;
+  if (fv_status s = check_embed_args(raw, xy, offsets, batch, n_total, img_wh, pca_mean, pca_basis, m)) return s;
+  if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags, false)) return s;
+  if (std::isnan(thr) || thr >= 1.f) return fail(FV_ERR_ARG, "threshold must be < 1 and not NaN");
+  if (batch > 0 && !out) return fail(FV_ERR_ARG, "null out");
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  const int ldx = kEmbLd(m);
+  if (!make_layout(n_total, batch, K, D, false, L, 0, false, ldx)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  float *Xe = (float *)at(ws, L.emb);
+  if (fv_status s = launch_embed(raw, xy, offsets, batch, n_total, img_wh, pca_mean, pca_basis, m, Xe, ldx, st))
+    return s;
+  return encode_batched_impl(Xe, offsets, batch, n_total, D, w, mu, sg, K, thr, flags, out, ws, ws_bytes, st, &L,
+                             Scoring(), ldx);
 }
 
 int fv_last_launch_count(void) { return g_launches; }

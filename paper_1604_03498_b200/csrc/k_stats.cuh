@@ -89,6 +89,7 @@ struct Stats2Params {
   float *loglik_out;          // n_total (optional): per-descriptor log2 sum_j 2^(L_ij + b_j) (EM E-step)
   long long *trace;           // debug (GPUFV_TRACE builds): per-tile phase clocks of CTA 0
   int batch, D, K, Kp;
+  int ldx;                    // row stride of X in floats (>= D, % 4 == 0)
   float threshold;
   int gamma_mode;
 };
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   if (warp == kWarpTma) {
     // ======================================================= tile walk + X producer (TMA)
     if (lane == 0 && n > 0) {
-      const int Dv = p.D;
+      const int Dv = p.ldx;
       TileWalker tw, twp;  // box walker, L2-prefetch walker (4 tiles ahead)
       tw.init(p, t0, t1);
       twp.init(p, t0, t1);

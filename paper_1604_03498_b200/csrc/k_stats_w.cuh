@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
     // box b (dims 32 b ..) of every tile goes through stage b & 1; the k-th use of a stage has parity
     // k & 1 = (b >> 1) & 1, so each stage alternates phases 0, 1 within every tile.
     if (lane == 0 && n > 0) {
-      const int Dv = p.D;
+      const int Dv = p.ldx;
       TileWalker tw, twp;
       tw.init(p, t0, t1);
       twp.init(p, t0, t1);

@@ -117,3 +117,13 @@ def test_scored_workspace_grows_with_classes(lib):
     a, b = f(10000, 100, 256, 64, 1, 0, 0), f(10000, 100, 256, 64, 32, 0, 0)
     assert (a == 0 and b == 0) or b > a
     assert f(10000, 100, 256, 64, 0, 0, 0) == 0 and f(10000, 100, 256, 64, 33, 0, 0) == 0
+
+
+@pytest.mark.parametrize("m,ldx,status", [(0, 4, 1), (127, 132, 1), (80, 80, 1), (80, 82, 1)])
+def test_embed_argument_validation(lib, m, ldx, status):
+    f = lib.fv_embed
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
+                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    p = lambda v: ctypes.c_void_p(v * 4096)
+    assert f(p(1), p(1), p(1), 1, 10, p(1), p(1), p(1), m, p(1), ldx, None) == status

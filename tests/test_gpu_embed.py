@@ -1,0 +1,74 @@
+"""GPU parity of the PCA + xy embedding and of the raw-descriptor
+-> FV path (embed + encode at D = m + 2 = 82, the paper's descriptor format) against the fp64
+oracle (oracle.embed, then oracle.encode on the oracle's embedding).
+
+Tolerances: the embedding accumulates 128 fp32 products per output, so |err| <= 128 * 2^-24 * sum_k
+|b_ck (d_k - mean_k)| <= 1e-5 ||d - mean|| (Cauchy-Schwarz, orthonormal rows); the FV bound is
+north_star's 1e-4 relative L2 (the fp32 embedding moves the encoder input by ~1e-7 relative)."""
+import numpy as np
+import pytest
+import torch
+
+import fvgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fv():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1604_03498_b200 as m
+    return m
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("m,counts", [(80, [5000, 1, 0, 333]), (62, [1000, 2049]), (7, [130, 64])])
+def test_embed_matches_oracle(fv, m, counts):
+    mean, B = fvgen.make_pca(m, seed=11)
+    gmm = fvgen.make_embedded_gmm(16, m, seed=12)
+    raw, xy, off, wh = fvgen.make_raw_frames(gmm, (mean, B), counts, seed=13, img_wh=(320, 240))
+    wh[-1] = [640, 480]
+    E = fv.embed(dev(raw), dev(xy), dev(off), dev(wh), dev(mean), dev(B)).cpu().numpy()
+    ref = oracle.embed(raw, xy, off, wh, mean, B)
+    ld = (m + 2 + 3) // 4 * 4
+    assert E.shape == (raw.shape[0], ld)
+    bound = 1e-5 * np.linalg.norm(raw.astype(np.float64) - mean, axis=1)[:, None] + 1e-30
+    assert np.all(np.abs(E[:, :m] - ref[:, :m]) <= bound)
+    np.testing.assert_allclose(E[:, m:m + 2], ref[:, m:], rtol=1e-7)
+    assert np.all(E[:, m + 2:] == 0)
+
+
+@pytest.mark.parametrize("tau", [0.0, 1e-6])
+def test_raw_to_fv_d82_matches_oracle(fv, tau):
+    """One 320x240 frame of 5000 raw descriptors + a 700-descriptor image, K=256, m=80 -> D=82 (wide
+    kernel, D not a multiple of 4 through the padded row stride)."""
+    m, K = 80, 256
+    mean, B = fvgen.make_pca(m, seed=21)
+    gmm_np = fvgen.make_embedded_gmm(K, m, seed=22)
+    raw, xy, off, wh = fvgen.make_raw_frames(gmm_np, (mean, B), [5000, 700], seed=23)
+    gmm = fv.GMM(*gmm_np)
+    out = fv.embed_encode_batched(dev(raw), dev(xy), dev(off), dev(wh), dev(mean), dev(B), gmm,
+                                  threshold=tau).cpu().numpy()
+    E = oracle.embed(raw, xy, off, wh, mean, B)
+    ref = oracle.encode_batched(E, off, *gmm_np, threshold=tau)
+    rel = np.linalg.norm(out - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    print(f"D=82 tau={tau}: rel-L2 {rel}")
+    assert out.shape == (2, 2 * K * 82) and np.all(rel < 1e-4)
+
+
+def test_raw_to_fv_narrow_d64(fv):
+    """m = 62 -> D = 64: the narrow kernel behind the embedding."""
+    m, K = 62, 128
+    mean, B = fvgen.make_pca(m, seed=31)
+    gmm_np = fvgen.make_embedded_gmm(K, m, seed=32)
+    raw, xy, off, wh = fvgen.make_raw_frames(gmm_np, (mean, B), [3000, 2500], seed=33)
+    out = fv.embed_encode_batched(dev(raw), dev(xy), dev(off), dev(wh), dev(mean), dev(B), fv.GMM(*gmm_np),
+                                  threshold=1e-6).cpu().numpy()
+    ref = oracle.encode_batched(oracle.embed(raw, xy, off, wh, mean, B), off, *gmm_np, threshold=1e-6)
+    rel = np.linalg.norm(out - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert np.all(rel < 1e-4)
