@@ -751,7 +751,7 @@ fv_status launch_embed(const float *raw, const float *xy, const int64_t *offsets
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t ntiles = (n_total + kEmbRows - 1) / kEmbRows;
-  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * 2);
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * (smem <= 75 * 1024 ? 3 : 2));
   k_embed<<<grid, 256, smem, st>>>(e);
   g_launches += 1;
   return cuda_check("k_embed");

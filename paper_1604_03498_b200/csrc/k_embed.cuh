@@ -58,23 +58,25 @@ __global__ void __launch_bounds__(256) k_embed(const EmbedParams p) {
     }
     __syncthreads();
     if (tid < nthr) {
-      float acc[4][8];
+      float2 acc[4][4];  // packed fp32x2 accumulators: columns 8 cg + 2 c, + 1
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
+        for (int c = 0; c < 4; ++c) acc[i][c] = make_float2(0.f, 0.f);
       const float *xa = Xs + rg * kEmbXStride;
       const float *ba = Bs + 8 * cg;
 #pragma unroll 4
       for (int k = 0; k < kEmbIn; ++k) {
         const float4 b0 = *reinterpret_cast<const float4 *>(ba + k * p.mpad);
         const float4 b1 = *reinterpret_cast<const float4 *>(ba + k * p.mpad + 4);
-        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        const float2 bb[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                              make_float2(b1.z, b1.w)};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float x = xa[16 * i * kEmbXStride + k];
+          const float2 xx = make_float2(x, x);
 #pragma unroll
-          for (int c = 0; c < 8; ++c) acc[i][c] = fmaf(x, bb[c], acc[i][c]);
+          for (int c = 0; c < 4; ++c) acc[i][c] = __ffma2_rn(xx, bb[c], acc[i][c]);
         }
       }
 #pragma unroll
@@ -83,12 +85,12 @@ __global__ void __launch_bounds__(256) k_embed(const EmbedParams p) {
         if (r >= nr) continue;
         float *o = p.out + (size_t)(r0 + r) * p.ldx + 8 * cg;
         if (8 * cg + 8 <= p.m) {
-          reinterpret_cast<float4 *>(o)[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-          reinterpret_cast<float4 *>(o)[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+          reinterpret_cast<float4 *>(o)[0] = make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
+          reinterpret_cast<float4 *>(o)[1] = make_float4(acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
         } else {
 #pragma unroll
           for (int c = 0; c < 8; ++c)
-            if (8 * cg + c < p.m) o[c] = acc[i][c];
+            if (8 * cg + c < p.m) o[c] = (c & 1) ? acc[i][c >> 1].y : acc[i][c >> 1].x;
         }
       }
     }
