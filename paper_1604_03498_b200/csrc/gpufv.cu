@@ -318,7 +318,9 @@ fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStrea
   for (int b0 = 0; b0 < batch; b0 += 65535) {  // gridDim.y limit
     FinParams fc = f;
     fc.b_base = b0;
-    k_finalize<<<dim3((K + kFinJ - 1) / kFinJ, std::min(65535, batch - b0), (D + kDP - 1) / kDP), 256, 0, st>>>(fc);
+    const dim3 grid((K + kFinJ - 1) / kFinJ, std::min(65535, batch - b0), (D + kDP - 1) / kDP);
+    if (f.n_cls > 0) k_finalize<true><<<grid, 256, 0, st>>>(fc);
+    else k_finalize<false><<<grid, 256, 0, st>>>(fc);
     g_launches += 1;
   }
   return cuda_check("k_finalize");

@@ -270,6 +270,7 @@ __device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int 
 // block order, divides by the image's norm and adds the bias (bitwise repeatable, no atomics).  With
 // out == nullptr only the scores leave the kernel (the FV is never written to HBM).
 constexpr int kFinKR = 2;  // dims per thread (kr, kr + 32)
+template <bool kScore>  // kScore = false: the plain encode (no scoring code compiled in)
 __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
   __shared__ double s_red[8];
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   }
   __syncthreads();
   const int part = blockIdx.z * gridDim.x + blockIdx.x, nparts = gridDim.x * gridDim.z;
-  if (p.out) {
+  if (!kScore || p.out) {
     float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D + kb;
     for (int t = tid; t < nj * nk; t += 256) {
       const int r = t / nk, k = t - r * nk;
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
       o[KD + (size_t)r * p.D + k] = sV[r][k];
     }
   }
-  if (p.n_cls > 0) {
+  if (kScore) {
     // this thread's tile elements t = tid + 256 u (nj * nk <= 2048), classifier reads coalesced over t
     constexpr int kE = kFinJ * kDP / 256;
     float zu[kE], zv[kE];
@@ -460,7 +461,7 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
     }
   }
   const bool l2 = p.mode != 2;
-  if (!l2 && p.n_cls == 0) return;
+  if (!kScore && !l2) return;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
   if ((tid & 31) == 0) s_red[tid >> 5] = ss;
@@ -479,13 +480,13 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   double n2 = 0.0;  // fixed-order sum of the parts: bitwise repeatable
   if (l2)
     for (int k = 0; k < nparts; ++k) n2 += __ldcg(p.norm2 + (size_t)b * kFinMaxParts + k);
-  if (tid < p.n_cls) {  // scores of the normalised FV (an all-zero FV scores the bias)
+  if (kScore && tid < p.n_cls) {  // scores of the normalised FV (an all-zero FV scores the bias)
     double d = 0.0;
     for (int k = 0; k < nparts; ++k) d += __ldcg(p.spart + ((size_t)b * kFinMaxParts + k) * p.n_cls + tid);
     const double inv = l2 ? (n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0) : 1.0;
     p.scores[(size_t)b * p.n_cls + tid] = (float)(d * inv + (p.svm_b ? (double)p.svm_b[tid] : 0.0));
   }
-  if (!l2 || !p.out || !(n2 > 0.0)) return;
+  if (!l2 || (kScore && !p.out) || !(n2 > 0.0)) return;
   const float sc = (float)(1.0 / sqrt(n2));
   float4 *ob = reinterpret_cast<float4 *>(p.out + (size_t)b * 2 * KD);  // 2KD % 4 == 0 (D % 4 == 0)
   const int n4 = (2 * KD) / 4;

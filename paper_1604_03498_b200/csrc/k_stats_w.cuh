@@ -48,7 +48,7 @@ static_assert(kSmemWBytes <= 232448, "shared memory budget (wide)");
 
 enum : int {
   W_XFULL0 = 0, W_XFULL1, W_XEMPTY0, W_XEMPTY1, W_ZR_FULL, W_G1_DONE, W_G2A_DONE, W_G2_DONE,
-  W_L_EMPTY, W_P_FULL, W_ZB_FULL, W_FOLD_DONE, W_XCHG0, W_XCHG1, W_W_FULL
+  W_L_EMPTY, W_P_FULL, W_ZB_FULL, W_FOLD_DONE, W_XCHG0, W_XCHG1, W_W_FULL, W_ZRA_FULL
 };
 
 // tensor-memory columns: Zr (half hf at 128 hf), L (64), S'_hf (64 each)
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
   if (tid == 0) {
     mbar_init(&bars[W_XFULL0], 1); mbar_init(&bars[W_XFULL1], 1);
     mbar_init(&bars[W_XEMPTY0], kWarpsWork); mbar_init(&bars[W_XEMPTY1], kWarpsWork);
-    mbar_init(&bars[W_ZR_FULL], kWarpsWork);
+    mbar_init(&bars[W_ZR_FULL], kWarpsWork); mbar_init(&bars[W_ZRA_FULL], kWarpsWork);
     mbar_init(&bars[W_G1_DONE], 1); mbar_init(&bars[W_G2A_DONE], 1); mbar_init(&bars[W_G2_DONE], 1);
     mbar_init(&bars[W_L_EMPTY], kWarpsWork); mbar_init(&bars[W_P_FULL], kWarpsWork);
     mbar_init(&bars[W_ZB_FULL], kWarpsWork); mbar_init(&bars[W_FOLD_DONE], kWarpsWork);
@@ -149,25 +149,35 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       const uint32_t idesc2 = idesc_f16_f32(kNF, kGW, 1, 1);  // A = Z_hf^T (SMEM, MN-major), B = P MN-major
       uint32_t folds = 0;
       mbar_wait(&bars[W_W_FULL], 0);
-      auto gemm1 = [&](int i) {
-        mbar_wait(&bars[W_ZR_FULL], i & 1);
+      auto g1 = [&](int s, int hf) {  // one split product of one feature half into L
+        const uint32_t za = tmem + kWTZr + 128 * hf + (s == 1 ? 64 : 0);           // hi, lo, hi
+        const uint32_t wb = sW + hf * (kWImgBytes / 2) + (s == 0 ? kGW * 128 * 2 : 0);  // lo, hi, hi
+        const bool first = (s == 0 && hf == 0);
+#pragma unroll
+        for (int kk = 0; kk < kNF / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (kGW * 128) + (kk & 3) * 32;
+          mma_f16_ts(tmem + kWTL, za + kk * 8, desc_sw128(wb + off, 16, 1024), idesc1, (first && kk == 0) ? 0u : 1u);
+        }
+      };
+      // GEMM1 in two parts so half a's cross terms run while half b is still being converted; all
+      // cross terms precede the hi.hi terms (truncating accumulator): (s0,a) (s1,a) | (s0,b) (s1,b) (s2,a) (s2,b)
+      auto gemm1a = [&](int i) {
+        mbar_wait(&bars[W_ZRA_FULL], i & 1);
         if (i >= 1) mbar_wait(&bars[W_L_EMPTY], (i - 1) & 1);
         tc_fence_after();
-#pragma unroll 1
-        for (int s = 0; s < 3; ++s) {  // cross terms first, hi.hi last (truncating accumulator)
-#pragma unroll 1
-          for (int hf = 0; hf < 2; ++hf) {
-            const uint32_t za = tmem + kWTZr + 128 * hf + (s == 1 ? 64 : 0);           // hi, lo, hi
-            const uint32_t wb = sW + hf * (kWImgBytes / 2) + (s == 0 ? kGW * 128 * 2 : 0);  // lo, hi, hi
-#pragma unroll
-            for (int kk = 0; kk < kNF / 16; ++kk) {
-              const uint32_t off = (kk >> 2) * (kGW * 128) + (kk & 3) * 32;
-              mma_f16_ts(tmem + kWTL, za + kk * 8, desc_sw128(wb + off, 16, 1024), idesc1, (s | hf | kk) != 0);
-            }
-          }
-        }
+        g1(0, 0);
+        g1(1, 0);
+      };
+      auto gemm1b = [&](int i) {
+        mbar_wait(&bars[W_ZR_FULL], i & 1);
+        tc_fence_after();
+        g1(0, 1);
+        g1(1, 1);
+        g1(2, 0);
+        g1(2, 1);
         mma_commit(&bars[W_G1_DONE]);
       };
+      auto gemm1 = [&](int i) { gemm1a(i); gemm1b(i); };
       auto gemm2 = [&](int hf, bool chunk_first) {  // S'_hf (+)= Z_hf^T P over the tile's 128 rows
         tc_fence_after();
 #pragma unroll 1
@@ -191,12 +201,13 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         gemm2(0, chunk_first);
         mma_commit(&bars[W_G2A_DONE]);
         TR(11);
+        if (i + 1 < n) gemm1a(i + 1);        // Zr(i+1) half a is converted before Z_b(i) is copied
         mbar_wait(&bars[W_ZB_FULL], i & 1);  // Z_b(i)
         TR(12);
         gemm2(1, chunk_first);
         mma_commit(&bars[W_G2_DONE]);
         TR(13);
-        if (i + 1 < n) gemm1(i + 1);
+        if (i + 1 < n) gemm1b(i + 1);
         TR(14);
       }
     }
@@ -222,12 +233,12 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
           zr_box<true>(xbox, row, bl, h, p.D - kDP * hf, row < nrows, s_sc + kDP * hf, s_ncs + kDP * hf, ta);
         else
           zr_box<false>(xbox, row, bl, h, kDP, true, s_sc + kDP * hf, s_ncs + kDP * hf, ta);
-        if (hf == 1 && bl == 1) tmem_st_wait();
+        if (bl == 1) tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&bars[W_XEMPTY0 + st]);
-          if (hf == 1 && bl == 1) mbar_arrive(&bars[W_ZR_FULL]);
+          if (bl == 1) mbar_arrive(&bars[hf == 1 ? W_ZR_FULL : W_ZRA_FULL]);
         }
       }
     };

@@ -101,12 +101,14 @@ capture("finalize", "k_finalize on C4",
         f"{NC} -k regex:k_finalize -s 3 -c 1 python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-latency --cpu-seconds 0")
 capture("kstats_w", "k_stats_w (wide, D=128, K=512) on a 2M-row C5 set",
         f"{NC} -k regex:k_stats_w -s 3 -c 1 python bench.py --workload c5 --c5-n 2000000 --steps 1 --warmup 3 --e2e-steps 0")
+capture("embed", "k_embed (PCA m=80 + xy, 256 frames x 5000 raw descriptors)",
+        f"{NC} -k regex:k_embed -s 3 -c 1 python bench.py --workload embed --frames 256 --steps 1 --warmup 3")
 n_total = 4096 * 5000
 with open(os.path.join(out_dir, "kstats_traffic.json"), "w") as f:
     json.dump({"tag": tag, "n_total": n_total, "dram_bytes_per_launch": dram,
                "source": f"profiles/{tag}_kstats_ncu.md"}, f, indent=1)
 print(open(os.path.join(out_dir, f"{tag}_launch_list.md")).read()[:1500])
-for nm in ("kstats", "finalize", "kstats_w"):
+for nm in ("kstats", "finalize", "kstats_w", "embed"):
     pth = os.path.join(out_dir, f"{tag}_{nm}_ncu.md")
     if os.path.exists(pth):
         print(open(pth).read())

@@ -1,7 +1,7 @@
 #!/usr/bin/env bash
 # Run on the GPU box (gpurun): launch list of the bench command + ncu --set full captures of the
-# stats kernel on the full C4 workload, of k_finalize (C4), and of the wide stats kernel (C5 shape,
-# 2M rows).  Outputs land in gpurun_out/ (scratch); tools/ncu_summary.py turns them into the
+# stats kernel on the full C4 workload, of k_finalize (C4), of the wide stats kernel (C5 shape,
+# 2M rows) and of k_embed (raw -> D=82 embedding, 256 frames).  Outputs land in gpurun_out/ (scratch); tools/ncu_summary.py turns them into the
 # committed profiles/ summaries.
 set -u
 TAG=${1:-r01}
@@ -22,3 +22,7 @@ timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k re
   -o gpurun_out/${TAG}_kstats_w python bench.py --workload c5 --c5-n 2000000 --steps 1 --warmup 3 --e2e-steps 0 \
   > gpurun_out/${TAG}_kstats_w.log 2>&1
 tail -1 gpurun_out/${TAG}_kstats_w.log
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_embed -s 3 -c 1 \
+  -o gpurun_out/${TAG}_embed python bench.py --workload embed --frames 256 --steps 1 --warmup 3 \
+  > gpurun_out/${TAG}_embed.log 2>&1
+tail -1 gpurun_out/${TAG}_embed.log
