@@ -47,6 +47,18 @@ fv_status cuda_check(const char *what) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+int sm_count() {
+  static int cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
 // Tile family: D <= 64 -> k_stats (128 Gaussians per CTA, cluster <= 4); 64 < D <= 128 -> k_stats_w
 // (64 Gaussians per CTA, cluster <= 8).  K <= 512 for both.
 constexpr int kMinTilesPerCluster = 4;
@@ -208,8 +220,9 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   if (ldx <= 0) ldx = D;
   // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
   int64_t *off1 = (int64_t *)at(ws, L.off1);
+  unsigned *counters = (unsigned *)((double *)at(ws, L.norm2) + (size_t)(batch > 0 ? batch : 1) * kFinMaxParts);
   k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles), L.ncl,
-                                 (int *)at(ws, L.cstart), (int *)at(ws, L.cown));
+                                 (int *)at(ws, L.cstart), (int *)at(ws, L.cown), counters);
   if (!offsets) offsets = off1;
   g_launches += 1;
   Stats2Params p;
@@ -254,17 +267,19 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
     if (r != CUDA_SUCCESS) return fail(FV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   }
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = L.C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps k_schedule
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3(L.C * L.ncl, 1, 1);
   cfg.blockDim = dim3(kThreads2, 1, 1);
   cfg.dynamicSmemBytes = is_wide(K, D) ? kSmemWBytes : kSmem2Bytes;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (g_prof_start) cudaEventRecord(g_prof_start, st);
   cudaError_t e;
   if (!is_wide(K, D)) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false>, tmap, p);
@@ -311,16 +326,32 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   return f;
 }
 
-fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStream_t st) {
-
+// after_stats: launched right behind k_stats (whose k_schedule zeroed the counters): programmatic
+// launch, no memset node in between.  Otherwise (fv_finalize from statistics) the counters are zeroed here.
+fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStream_t st, bool after_stats = true) {
   if (batch == 0) return FV_OK;
-  if (cudaMemsetAsync(f.counters, 0, (size_t)batch * 4, st) != cudaSuccess) return cuda_check("memset tickets");
+  if (!after_stats && cudaMemsetAsync(f.counters, 0, (size_t)batch * 4, st) != cudaSuccess)
+    return cuda_check("memset tickets");
   for (int b0 = 0; b0 < batch; b0 += 65535) {  // gridDim.y limit
     FinParams fc = f;
     fc.b_base = b0;
     const dim3 grid((K + kFinJ - 1) / kFinJ, std::min(65535, batch - b0), (D + kDP - 1) / kDP);
-    if (f.n_cls > 0) k_finalize<true><<<grid, 256, 0, st>>>(fc);
-    else k_finalize<false><<<grid, 256, 0, st>>>(fc);
+    // one wave (every block resident at once: <= 1 block per SM): blocks wait for their image's
+    // siblings and write once (latency path); otherwise the last block of each image rescales it
+    const bool sync = (int64_t)grid.x * grid.y * grid.z <= (int64_t)sm_count();
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (after_stats && b0 == 0) ? 1 : 0;
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    if (f.n_cls > 0) e = sync ? cudaLaunchKernelEx(&cfg, k_finalize<true, true>, fc) : cudaLaunchKernelEx(&cfg, k_finalize<true, false>, fc);
+    else e = sync ? cudaLaunchKernelEx(&cfg, k_finalize<false, true>, fc) : cudaLaunchKernelEx(&cfg, k_finalize<false, false>, fc);
+    if (e != cudaSuccess) return fail(FV_ERR_CUDA, "k_finalize launch: %s", cudaGetErrorString(e));
     g_launches += 1;
   }
   return cuda_check("k_finalize");
@@ -588,7 +619,7 @@ fv_status fv_finalize(const double *stats, int batch, int D, const float *w, con
   f.slots = nullptr;
   f.stats = stats;
   f.out = out;
-  return launch_finalize(f, batch, K, D, st);
+  return launch_finalize(f, batch, K, D, st, false);
 }
 
 fv_status fv_posteriors(const float *X, int64_t N, int D, const float *w, const float *mu, const float *sg, int K,

@@ -9,6 +9,7 @@
 #pragma once
 #include <cuda_fp16.h>
 #include "fv_common.cuh"
+#include "ptx.cuh"
 
 namespace gpufv {
 
@@ -137,11 +138,15 @@ __device__ __forceinline__ int64_t tile_owner(int64_t t, int64_t T, int64_t ncl)
 // Also the static split of the T tiles over the ncl clusters, for the finalize (no divisions there):
 //   cstart[c] = c T / ncl (c = 0..ncl);  cown[2b], cown[2b+1] = first / last cluster owning a tile of
 //   image b (last < first for an empty image).
+// Also zeroes the finalize's per-image arrival counters (so no memset node separates k_stats from
+// k_finalize in the stream) and lets k_stats start its prologue early (programmatic launch).
 __global__ void k_schedule(const int64_t *offsets, int64_t *off1, int64_t n_single, int batch, int64_t *tile_start,
-                           int ncl, int *cstart, int *cown) {
+                           int ncl, int *cstart, int *cown, unsigned *counters) {
   __shared__ int64_t s_warp[32];
   __shared__ int64_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  ptx::griddep_launch_dependents();
+  for (int b = tid; b < batch; b += 1024) counters[b] = 0u;
   if (!offsets) {
     if (tid == 0) {
       off1[0] = 0; off1[1] = n_single;
@@ -270,8 +275,13 @@ __device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int 
 // block order, divides by the image's norm and adds the bias (bitwise repeatable, no atomics).  With
 // out == nullptr only the scores leave the kernel (the FV is never written to HBM).
 constexpr int kFinKR = 2;  // dims per thread (kr, kr + 32)
-template <bool kScore>  // kScore = false: the plain encode (no scoring code compiled in)
+// kSync (small launches, all blocks co-resident: the host uses it when the grid fits in one wave):
+// every block of an image publishes its partial sum of squares, waits for its siblings and writes its
+// tile once, already scaled — no serial rescale of the whole image by its last block (the latency
+// path).  For large batches the last-block variant wins (waiting blocks would hold slots).
+template <bool kScore, bool kSync>  // kScore = false: the plain encode (no scoring code compiled in)
 __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
+  ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
   __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
   __shared__ double s_red[8];
   __shared__ float s_dot[8][kMaxCls];
@@ -418,7 +428,7 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   }
   __syncthreads();
   const int part = blockIdx.z * gridDim.x + blockIdx.x, nparts = gridDim.x * gridDim.z;
-  if (!kScore || p.out) {
+  if (!kSync && (!kScore || p.out)) {
     float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D + kb;
     for (int t = tid; t < nj * nk; t += 256) {
       const int r = t / nk, k = t - r * nk;
@@ -461,6 +471,48 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
     }
   }
   const bool l2 = p.mode != 2;
+  if (kSync) {
+    float sc = 1.f;
+    if (l2 || kScore) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      if ((tid & 31) == 0) s_red[tid >> 5] = ss;
+      __syncthreads();
+      if (tid == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < 8; ++w) tot += s_red[w];
+        p.norm2[(size_t)b * kFinMaxParts + part] = tot;  // own slot
+      }
+      __threadfence();  // this block's norm / score parts before its arrival
+      __syncthreads();
+      if (tid == 0) {
+        unsigned *ctr = p.counters + b;
+        atomicAdd(ctr, 1u);
+        while (atomicAdd(ctr, 0u) < (unsigned)nparts) __nanosleep(32);
+        __threadfence();
+      }
+      __syncthreads();
+      double n2 = 0.0;  // fixed-order sum of the parts: the same bits in every block
+      if (l2)
+        for (int k = 0; k < nparts; ++k) n2 += __ldcg(p.norm2 + (size_t)b * kFinMaxParts + k);
+      if (l2 && n2 > 0.0) sc = (float)(1.0 / sqrt(n2));
+      if (kScore && part == 0 && tid < p.n_cls) {
+        double d = 0.0;
+        for (int k = 0; k < nparts; ++k) d += __ldcg(p.spart + ((size_t)b * kFinMaxParts + k) * p.n_cls + tid);
+        const double inv = l2 ? (n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0) : 1.0;
+        p.scores[(size_t)b * p.n_cls + tid] = (float)(d * inv + (p.svm_b ? (double)p.svm_b[tid] : 0.0));
+      }
+    }
+    if (!kScore || p.out) {
+      float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D + kb;
+      for (int t = tid; t < nj * nk; t += 256) {
+        const int r = t / nk, k = t - r * nk;
+        o[(size_t)r * p.D + k] = sU[r][k] * sc;
+        o[KD + (size_t)r * p.D + k] = sV[r][k] * sc;
+      }
+    }
+    return;
+  }
   if (!kScore && !l2) return;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
@@ -488,7 +540,12 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   }
   if (!l2 || (kScore && !p.out) || !(n2 > 0.0)) return;
   const float sc = (float)(1.0 / sqrt(n2));
-  float4 *ob = reinterpret_cast<float4 *>(p.out + (size_t)b * 2 * KD);  // 2KD % 4 == 0 (D % 4 == 0)
+  if ((2 * KD) % 4 != 0) {  // any D (the embedding path): scalar rescale
+    float *o1 = p.out + (size_t)b * 2 * KD;
+    for (int t = tid; t < 2 * KD; t += 256) o1[t] = __ldcg(o1 + t) * sc;
+    return;
+  }
+  float4 *ob = reinterpret_cast<float4 *>(p.out + (size_t)b * 2 * KD);  // 2KD % 4 == 0
   const int n4 = (2 * KD) / 4;
   for (int t0 = 0; t0 < n4; t0 += 256 * 8) {  // 8 loads in flight per thread (the image is in L2)
     float4 v[8];

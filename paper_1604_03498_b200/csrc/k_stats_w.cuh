@@ -103,6 +103,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
   cluster_sync();
+  griddep_launch_dependents();  // k_finalize may start its prologue
+  griddep_wait();               // k_schedule's tile prefix sums are complete and visible
 
   const int64_t T = p.tile_start[p.batch];
   const int t0 = (int)((int64_t)cid * T / ncl), t1 = (int)((int64_t)(cid + 1) * T / ncl);

@@ -236,6 +236,12 @@ __device__ __forceinline__ void st_cluster_v2f32(uint32_t addr, float a, float b
 }
 
 // ------------------------------------------------------------------ math
+// Programmatic dependent launch (sm_90+): let the next kernel in the stream start its prologue, and
+// wait for the previous kernel's completion + memory flush before consuming its results.  Both are
+// no-ops when the kernel was not launched with the programmatic-serialization attribute.
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
