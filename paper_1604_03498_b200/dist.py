@@ -133,3 +133,33 @@ def em_step_sharded(X_shard, gmm, group=None, estep_fn=None, mstep_fn=None, dete
         else:
             dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     return mstep_fn(buf[:-1].contiguous()), float(buf[-1].item())
+
+
+def score_frames_sharded(X, offsets, gmm, svm_w, svm_b=None, threshold: float = 0.0, mode: int = 0, group=None,
+                         score_fn=None, gather: bool = True):
+    """Frame-sharded monitoring (NEXT-4): rank r scores frames shard_ranges(B, world)[r] with
+    the classifier fused into the finalize (no FV leaves the GPU); only the (frames, n_cls) scores are
+    all-gathered (4 B per frame and class instead of 2KD floats)."""
+    import numpy as np
+
+    rank, world = _rank_world(group)
+    off = np.asarray(offsets, dtype=np.int64)
+    B = off.shape[0] - 1
+    lo, hi = shard_ranges(B, world)[rank]
+    r0, r1 = int(off[lo]), int(off[hi])
+    local_off = torch.from_numpy(off[lo:hi + 1] - r0)
+    if score_fn is None:
+        from . import encode_scored_batched as _sc
+
+        def score_fn(Xs, offs):
+            return _sc(Xs, offs.to(Xs.device), gmm, svm_w, svm_b, threshold=threshold, mode=mode)
+    s = score_fn(X[r0:r1], local_off)
+    if not gather or world == 1:
+        return s
+    sizes = [b - a for a, b in shard_ranges(B, world)]
+    mx = max(sizes)
+    padded = s.new_zeros((mx, s.shape[1]))
+    padded[:s.shape[0]] = s
+    buf = [s.new_zeros((mx, s.shape[1])) for _ in sizes]
+    dist.all_gather(buf, padded, group=group)
+    return torch.cat([t[:n] for t, n in zip(buf, sizes)], 0)

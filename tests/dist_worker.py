@@ -63,5 +63,11 @@ for det in (False, True):
         mstep_fn=mstep_from_stats, deterministic=det)
     res[f"em_pi_{det}"], res[f"em_mu_{det}"], res[f"em_var_{det}"] = new
     res[f"em_ll_{det}"] = np.array([ll])
+rng = np.random.default_rng(34)
+W = rng.standard_normal((3, 2 * 16 * 8))
+sc = fvd.score_frames_sharded(
+    Xb, off, gmm, W,
+    score_fn=lambda Xs, o: torch.from_numpy(oracle.score(oracle.encode_batched(Xs, o.numpy(), *gmm, threshold=1e-6), W)))
+res["scores"] = sc.numpy()
 np.savez(os.path.join(os.environ["OUT_DIR"], f"rank{rank}.npz"), **res)
 dist.destroy_process_group()

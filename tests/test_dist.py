@@ -87,3 +87,14 @@ def test_em_sharded_allreduce_equals_whole_set_em(results):
             np.testing.assert_allclose(results[r][f"em_mu_{det}"], mu, rtol=1e-9, atol=1e-12)
             np.testing.assert_allclose(results[r][f"em_var_{det}"], var, rtol=1e-8)
             assert results[r][f"em_ll_{det}"][0] == pytest.approx(ll, rel=1e-12)
+
+
+def test_frame_sharded_scores_gather(results):
+    """Monitoring (NEXT-4): per-rank fused scores all-gathered in frame order == scoring every FV."""
+    gmm = fvgen.make_gmm(16, 8, seed=31)
+    Xb, off = fvgen.make_batch(gmm, [10, 300, 0, 77, 5], seed_base=33)
+    W = np.random.default_rng(34).standard_normal((3, 2 * 16 * 8))
+    ref = oracle.score(oracle.encode_batched(Xb, off, *gmm, threshold=1e-6), W)
+    for r in (0, 1):
+        assert results[r]["scores"].shape == (5, 3)
+        np.testing.assert_allclose(results[r]["scores"], ref, rtol=1e-12, atol=1e-12)

@@ -246,3 +246,25 @@ def test_posterior_error_margin_large_set(fv):
     err = np.abs(g - oracle.posteriors(X, *gmm_np)).max()
     print(f"max |gamma err| over {g.size} posteriors: {err:.3e}")
     assert err <= 0.6 * GAMMA_ATOL
+
+
+def test_c4_stream_full_size_sampled(fv):
+    """C4: the full 4096-frame x 5000-descriptor stream (20.48 M rows, the bench's launch: one
+    fv_encode_batched call, tau = 1e-6); frames spread over the whole persistent schedule (first,
+    cluster-boundary region, middle, last) checked against the oracle one by one, every FV unit-norm,
+    and the call repeated bitwise."""
+    cfg = fvgen.CONFIGS["C4"]
+    gmm_np = fvgen.make_gmm(cfg["K"], cfg["D"], seed=cfg["seed_gmm"])
+    F, P = cfg["frames"], cfg["per_frame"]
+    X = fvgen.make_frames(gmm_np, F, P, seed=cfg["seed_data"])
+    off = np.arange(F + 1, dtype=np.int64) * P
+    Xd, offd, gmm = dev(X), dev(off), fv.GMM(*gmm_np)
+    out = fv.encode_batched(Xd, offd, gmm, threshold=TAU)
+    out2 = fv.encode_batched(Xd, offd, gmm, threshold=TAU)
+    assert torch.equal(out, out2)
+    out = out.cpu().numpy()
+    assert np.all(np.isfinite(out))
+    np.testing.assert_allclose(np.linalg.norm(out, axis=1), 1.0, atol=1e-5)
+    for f in (0, 1, 55, 56, 2048, 4095):
+        ref = oracle.encode(X[f * P:(f + 1) * P], *gmm_np, threshold=TAU)
+        assert rel_l2(out[f], ref) <= FV_RTOL
