@@ -29,17 +29,19 @@ lib.fv_encode_batched.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c
                                   ctypes.c_float, ctypes.c_uint, vp, vp, ctypes.c_size_t, vp]
 lib.fv_debug_trace.argtypes = [vp]
 F = int(os.environ.get("FRAMES", "512"))
-gmm = fvgen.make_gmm(256, 64, seed=1604)
+K, D = int(os.environ.get("TRACE_K", "256")), int(os.environ.get("TRACE_D", "64"))
+TAU = float(os.environ.get("TRACE_TAU", "1e-6"))
+gmm = fvgen.make_gmm(K, D, seed=1604)
 X = torch.from_numpy(fvgen.make_frames(gmm, F, 5000, seed=1604 + 20000)).cuda()
 off = torch.arange(F + 1, dtype=torch.int64, device="cuda") * 5000
 w, m, v = (torch.from_numpy(a).cuda() for a in gmm)
-nb = lib.fv_workspace_bytes(X.shape[0], F, 256, 64, 0)
+nb = lib.fv_workspace_bytes(X.shape[0], F, K, D, 0)
 ws = torch.empty(nb + 1024, dtype=torch.uint8, device="cuda")
 wsp = (ws.data_ptr() + 1023) // 1024 * 1024
-out = torch.empty(F, 2 * 256 * 64, device="cuda")
+out = torch.empty(F, 2 * K * D, device="cuda")
 tr = torch.zeros(8192, dtype=torch.int64, device="cuda")
-args = lambda: (vp(X.data_ptr()), vp(off.data_ptr()), F, X.shape[0], 64, vp(w.data_ptr()), vp(m.data_ptr()),
-                vp(v.data_ptr()), 256, ctypes.c_float(1e-6), 0, vp(out.data_ptr()), vp(wsp), nb, None)
+args = lambda: (vp(X.data_ptr()), vp(off.data_ptr()), F, X.shape[0], D, vp(w.data_ptr()), vp(m.data_ptr()),
+                vp(v.data_ptr()), K, ctypes.c_float(TAU), 0, vp(out.data_ptr()), vp(wsp), nb, None)
 assert lib.fv_encode_batched(*args()) == 0
 lib.fv_debug_trace(vp(tr.data_ptr()))
 assert lib.fv_encode_batched(*args()) == 0
