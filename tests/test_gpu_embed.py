@@ -72,3 +72,18 @@ def test_raw_to_fv_narrow_d64(fv):
     ref = oracle.encode_batched(oracle.embed(raw, xy, off, wh, mean, B), off, *gmm_np, threshold=1e-6)
     rel = np.linalg.norm(out - ref, axis=1) / np.linalg.norm(ref, axis=1)
     assert np.all(rel < 1e-4)
+
+
+@pytest.mark.parametrize("m,K", [(41, 33), (30, 256), (100, 64)])
+def test_raw_to_fv_odd_dims(fv, m, K):
+    """D = m + 2 not a multiple of 4 (43, 102) and odd K: the padded row stride carries the encoder, the
+    finalize rescales a 2KD that is not a multiple of 4 (scalar path); narrow (D <= 64) and wide."""
+    mean, B = fvgen.make_pca(m, seed=41)
+    gmm_np = fvgen.make_embedded_gmm(K, m, seed=42)
+    raw, xy, off, wh = fvgen.make_raw_frames(gmm_np, (mean, B), [1500, 0, 777, 2100], seed=43)
+    out = fv.embed_encode_batched(dev(raw), dev(xy), dev(off), dev(wh), dev(mean), dev(B), fv.GMM(*gmm_np),
+                                  threshold=1e-6).cpu().numpy()
+    ref = oracle.encode_batched(oracle.embed(raw, xy, off, wh, mean, B), off, *gmm_np, threshold=1e-6)
+    assert np.all(out[1] == 0)
+    for b in (0, 2, 3):
+        assert np.linalg.norm(out[b] - ref[b]) / np.linalg.norm(ref[b]) < 1e-4
