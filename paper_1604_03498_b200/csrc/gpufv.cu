@@ -107,7 +107,7 @@ int num_clusters(int C, bool wide) {
 struct Layout {
   int C, Kp, ncl, dpad;  // cluster size, padded K, clusters, padded D (64 | 128)
   int64_t n_total, nslots;                                         // segment slots (cluster, image)
-  size_t wimg, bias, xshift, xscale, cshift, bscratch, bmax, coef;  // prepared GMM (head of ws)
+  size_t wimg, bias, xshift, xscale, cshift, bscratch, bmax, pscale, xinv, coef;  // prepared GMM (head of ws)
   size_t tiles, off1, cstart, cown, norm2, s0slots, slots;  // per call
   size_t spart;                                           // fused scoring partial dots (n_cls > 0)
   size_t llrows, llparts, emstats;                        // EM: per-row log2-likelihoods, reduction, stats
@@ -137,7 +137,9 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.xscale = o;   o = align_up(o + kDMax * 4, 256);
   L.cshift = o;   o = align_up(o + kDMax * 8, 256);
   L.bscratch = o; o = align_up(o + (size_t)L.Kp * 8, 256);
-  L.bmax = o;     o = align_up(o + 8, 1024);
+  L.bmax = o;     o = align_up(o + 8, 256);
+  L.pscale = o;   o = align_up(o + (size_t)2 * L.Kp * 8, 256);
+  L.xinv = o;     o = align_up(o + kDMax * 8, 1024);
   L.coef = o;     o = align_up(o + (size_t)3 * kDMax * L.Kp * 8, 1024);
   L.tiles = o;    o = align_up(o + (size_t)(batch + 1) * 8, 256);
   L.off1 = o;     o = align_up(o + 16, 256);
@@ -206,7 +208,7 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
   const int sd = (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0;
   k_prep_shift<<<1, 256, 0, st>>>(w, mu, sg, K, D, L.Kp, sd, (double *)at(ws, L.cshift), (float *)at(ws, L.xshift),
                                   (float *)at(ws, L.xscale), (float *)at(ws, L.bias), (double *)at(ws, L.bscratch),
-                                  (double *)at(ws, L.bmax));
+                                  (double *)at(ws, L.bmax), (double *)at(ws, L.pscale), (double *)at(ws, L.xinv));
   k_prep_w<<<L.Kp, 2 * L.dpad, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
                                  at(ws, L.wimg), (double *)at(ws, L.coef), is_wide(K, D) ? 1 : 0);
   g_launches += 2;
@@ -313,6 +315,8 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.w = w;
   f.coef = (const double *)at(ws, L.coef);
   f.xscale = (const float *)at(ws, L.xscale);
+  f.pscale = (const double *)at(ws, L.pscale);
+  f.xinv = (const double *)at(ws, L.xinv);
   f.out = nullptr;
   f.stats_out = nullptr;
   f.norm2 = (double *)at(ws, L.norm2);

@@ -26,7 +26,7 @@ __device__ __forceinline__ double gmm_var(const float *sigmas, size_t i, bool st
 // in log2 units.  One block of 256 threads.
 __global__ void k_prep_shift(const float *w, const float *mu, const float *sg, int K, int D, int Kp,
                              int stddev, double *cshift, float *xshift, float *xscale, float *bias,
-                             double *bscratch, double *bmax_out) {
+                             double *bscratch, double *bmax_out, double *pscale, double *xinv) {
   __shared__ double s_c[kDMax];
   __shared__ double s_red[256];
   const int tid = threadIdx.x;
@@ -50,6 +50,12 @@ __global__ void k_prep_shift(const float *w, const float *mu, const float *sg, i
     cshift[tid] = c;
     xshift[tid] = (float)c;
     xscale[tid] = (float)sc;
+    xinv[tid] = 1.0 / ((double)kPScale * sc);  // undoes P = gamma 2^14 and the feature scale (exact)
+  }
+  // finalize prior scales of the improved FV (reading A9): 1/sqrt(pi_j), 1/sqrt(2 pi_j)
+  for (int j = tid; j < Kp; j += 256) {
+    pscale[j] = j < K ? 1.0 / sqrt((double)w[j]) : 0.0;
+    pscale[Kp + j] = j < K ? 1.0 / sqrt(2.0 * (double)w[j]) : 0.0;
   }
   __syncthreads();
   double bmax = -1e300;
@@ -203,6 +209,8 @@ struct FinParams {
   const float *w;
   const double *coef;         // 3 x kDMax x Kp (k_prep_w)
   const float *xscale;
+  const double *pscale;       // 2 x Kp: 1/sqrt(pi_j), 1/sqrt(2 pi_j) (k_prep_shift)
+  const double *xinv;         // kDMax: 1 / (2^14 2^e_k) (k_prep_shift)
   float *out;                 // batch x 2KD
   double *stats_out;          // k_reduce_stats output
   double *norm2;              // batch x kFinMaxParts: each block's partial sum of squares (fixed slots)
@@ -257,7 +265,7 @@ __device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int 
   for (int i = 0; i < kFinKI; ++i) {
     const int k = kq + 8 * i;
     if (k < p.D) {
-      const double xs = 1.0 / ((double)kPScale * (double)p.xscale[k]);  // powers of two: exact
+      const double xs = p.xinv[k];  // powers of two: exact
       S1[i] *= xs;
       S2[i] *= xs * xs * (double)kPScale;  // S2 carries 2^14 once and the feature scale twice
     }
@@ -360,7 +368,7 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
 #pragma unroll
       for (int r = 0; r < kFinKR; ++r) {
         const int k = kr + 32 * r;
-        const double xs = 1.0 / ((double)kPScale * (double)p.xscale[k]);  // powers of two: exact
+        const double xs = p.xinv[k];  // 1 / (2^14 2^e_k): powers of two, exact
 #pragma unroll
         for (int e = 0; e < 4; ++e) { S1[r][e] *= xs; S2[r][e] *= xs * xs * (double)kPScale; }
       }
@@ -383,13 +391,13 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
       }
     }
     double fu[4], fv[4];
+    const double invN = N > 0.0 ? 1.0 / N : 0.0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       fu[e] = fv[e] = 1.0;
       if (p.mode == 0 && N > 0.0 && jb + e < p.K) {
-        const double pj = (double)p.w[jb + e];
-        fu[e] = 1.0 / (N * sqrt(pj));
-        fv[e] = 1.0 / (N * sqrt(2.0 * pj));
+        fu[e] = invN * p.pscale[jb + e];           // 1 / (N sqrt(pi_j))
+        fv[e] = invN * p.pscale[p.Kp + jb + e];    // 1 / (N sqrt(2 pi_j))
       }
     }
     const bool zero = (p.mode != 2) && !(N > 0.0);
