@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -61,7 +62,17 @@ int sm_count() {
 
 // Tile family: D <= 64 -> k_stats (128 Gaussians per CTA, cluster <= 4); 64 < D <= 128 -> k_stats_w
 // (64 Gaussians per CTA, cluster <= 8).  K <= 512 for both.
-constexpr int kMinTilesPerCluster = 4;
+constexpr int kMinTilesPerClusterDefault = 4;
+constexpr int kMaxSegPerImage = 26;
+// GPUFV_MIN_TILES overrides it (latency experiments only); read once per process
+int min_tiles_per_cluster() {
+  static const int v = [] {
+    const char *e = std::getenv("GPUFV_MIN_TILES");
+    const int x = e ? std::atoi(e) : 0;
+    return x > 0 ? x : kMinTilesPerClusterDefault;
+  }();
+  return v;
+}
 bool is_wide(int K, int D) { return D > kDP || K > kG * kMaxC2; }
 int gauss_per_cta(int K, int D) { return is_wide(K, D) ? kGW : kG; }
 int cluster_size(int K, int D) { return (K + gauss_per_cta(K, D) - 1) / gauss_per_cta(K, D); }
@@ -123,10 +134,15 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.dpad = is_wide(K, D) ? kDMax : kDP;
   L.ncl = num_clusters(L.C, is_wide(K, D));
   if (L.ncl <= 0) return false;
-  // small launches (one frame): at least kMinTilesPerCluster tiles per cluster, so an image is split
+  // small launches (one frame): at least min_tiles_per_cluster() tiles per cluster, so an image is split
   // into fewer (cluster) segments for the finalize to combine; tiles <= n_total/128 + batch
   const int64_t tmax = n_total / kTileM + batch;
-  if (tmax > 0) L.ncl = (int)std::min<int64_t>(L.ncl, std::max<int64_t>(1, (tmax + kMinTilesPerCluster - 1) / kMinTilesPerCluster));
+  const int mt = min_tiles_per_cluster();
+  if (tmax > 0) L.ncl = (int)std::min<int64_t>(L.ncl, std::max<int64_t>(1, (tmax + mt - 1) / mt));
+  // ... and at most ~kMaxSegPerImage segments per image on average: the finalize of one image costs
+  // ~1 us per extra segment (measured: one 40,000-descriptor image 157 us over 74 clusters, 92 us
+  // over 26), so a single large image uses fewer, longer cluster ranges
+  if (batch > 0) L.ncl = (int)std::min<int64_t>(L.ncl, (int64_t)kMaxSegPerImage * batch);
   // one slot per (cluster, image) segment, index cid + b (seg_slot, fv_common.cuh)
   L.n_total = n_total;
   L.nslots = (int64_t)L.ncl + batch + 1;
