@@ -2,7 +2,7 @@
  * encoded against a 256-component GMM with fv_encode, device memory from the CUDA runtime.
  *
  *   nvcc -o encode_c examples/encode_c.c -Iinclude -Lpaper_1604_03498_b200 -lgpufv \
- *        -Xlinker -rpath=$PWD/paper_1604_03498_b200 && ./encode_c
+ *        -Xlinker -rpath=$PWD/paper_1604_03498_b200 && ./encode_c [K D N]
  *
  * Prints the FV's L2 norm (1 for the improved FV), its first components and the status string; exits
  * non-zero on any error. */
@@ -21,9 +21,9 @@ static double urand(unsigned long long *s) { /* xorshift64*: inputs only, no met
 }
 static double nrand(unsigned long long *s) { return sqrt(-2.0 * log(urand(s) + 1e-300)) * cos(6.283185307179586 * urand(s)); }
 
-int main(void) {
-  const int K = 256, D = 64;
-  const long long N = 5000;
+int main(int argc, char **argv) {
+  const int K = argc > 1 ? atoi(argv[1]) : 256, D = argc > 2 ? atoi(argv[2]) : 64;
+  const long long N = argc > 3 ? atoll(argv[3]) : 5000;
   unsigned long long seed = 1604;
   float *w = malloc(K * sizeof(float)), *mu = malloc((size_t)K * D * sizeof(float)), *var = malloc((size_t)K * D * sizeof(float));
   float *X = malloc((size_t)N * D * sizeof(float)), *fv = malloc((size_t)2 * K * D * sizeof(float));

@@ -75,6 +75,7 @@ constexpr uint32_t kTZr = 0, kTL = 256, kTS = 384;
 
 // named barriers (0 = __syncthreads)
 constexpr uint32_t kBarLane0 = 1;  // 1..4: the 4 WORK warps of a TMEM lane group (k_stats_w's quarter combine)
+constexpr uint32_t kBarXchgLocal = 5;  // the 16 WORK warps of a single-CTA cluster (k_stats, K <= 128)
 
 struct Stats2Params {
   const float *X;             // n_total x D (also behind the tensor map; used for L2 prefetch)
@@ -477,6 +478,10 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       const int par = i & 1;
       float2 *xb = s_xchg + par * (kMaxC2 * 4 * kTileM);
       auto send = [&](float ssum) {
+        if (C == 1) {  // a cluster of one CTA (K <= 128) has no DSMEM peer: local store + named barrier below
+          xb[(rank * 4 + h) * kTileM + row] = make_float2(m, ssum);
+          return;
+        }
         if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[B_XCHG0 + par], C * 4 * kTileM * 8);
         const uint32_t my = smem_u32(&xb[(rank * 4 + h) * kTileM + row]);
         const uint32_t mybar = smem_u32(&bars[B_XCHG0 + par]);
@@ -497,7 +502,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         send(exp_local());
       }
       TRW(4);
-      mbar_wait(&bars[B_XCHG0 + par], (i >> 1) & 1);
+      if (C > 1) mbar_wait(&bars[B_XCHG0 + par], (i >> 1) & 1);
+      else named_bar_sync(kBarXchgLocal, kWarpsWork * 32);
       TRW(12);
       float M = -3.0e38f, S = 0.f;
       {

@@ -30,3 +30,19 @@ def test_c_example_runs(tmp_path):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "||fv|| = 1.0000" in r.stdout and "FV_ERR_UNSUPPORTED" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+@pytest.mark.parametrize("shape", [("256", "64", "5000"), ("512", "128", "3000"), ("16", "36", "1000")])
+def test_compute_sanitizer_clean(tmp_path, tool, shape):
+    """compute-sanitizer memcheck / racecheck / synccheck / initcheck over the whole encode
+    (prep, schedule, persistent tcgen05 stats kernel, finalize) for the narrow, wide and masked-D
+    families report no error."""
+    exe = _build(tmp_path)
+    r = subprocess.run(["compute-sanitizer", "--tool", tool, exe, *shape], capture_output=True, text=True,
+                       timeout=900)
+    out = r.stdout + r.stderr
+    print(out[-2000:])
+    assert r.returncode == 0, out[-2000:]
+    assert ("ERROR SUMMARY: 0 errors" in out) or ("0 hazards displayed (0 errors, 0 warnings)" in out)
