@@ -2,6 +2,7 @@
 libgpufv.so here; runs on the GPU (unit-norm FV, synchronous error status)."""
 import os
 import subprocess
+import sys
 
 import pytest
 
@@ -45,4 +46,20 @@ def test_compute_sanitizer_clean(tmp_path, tool, shape):
     out = r.stdout + r.stderr
     print(out[-2000:])
     assert r.returncode == 0, out[-2000:]
+    assert ("ERROR SUMMARY: 0 errors" in out) or ("0 hazards displayed (0 errors, 0 warnings)" in out)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer_all_entry_points(tool):
+    """Every entry point (encode, host pipeline, stats/finalize, posteriors, scoring, EM, embedding) on
+    narrow, wide and masked-D shapes under compute-sanitizer (PyTorch's own kernels included)."""
+    import __graft_entry__
+    __graft_entry__.build()
+    r = subprocess.run(["compute-sanitizer", "--tool", tool, "--kernel-name", "kns=gpufv",
+                        sys.executable, os.path.join(ROOT, "tools", "sanitize_entrypoints.py")],
+                       capture_output=True, text=True, timeout=1500)
+    out = r.stdout + r.stderr
+    print(out[-3000:])
+    assert r.returncode == 0 and "entry points ok" in out, out[-3000:]
     assert ("ERROR SUMMARY: 0 errors" in out) or ("0 hazards displayed (0 errors, 0 warnings)" in out)
