@@ -350,6 +350,35 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
 // launch, no memset node in between.  Otherwise (fv_finalize from statistics) the counters are zeroed here.
 fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStream_t st, bool after_stats = true) {
   if (batch == 0) return FV_OK;
+  // large batches of narrow images: one persistent block per SM takes whole images (k_finalize_img)
+  if (D <= kDP && K <= kImgK && batch >= 2 * sm_count() && !std::getenv("GPUFV_FIN_TILES")) {
+    static bool attr_done = false;
+    if (!attr_done) {
+      if (cudaFuncSetAttribute(k_finalize_img<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgSmemBytes) !=
+              cudaSuccess ||
+          cudaFuncSetAttribute(k_finalize_img<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgSmemBytes) !=
+              cudaSuccess)
+        return cuda_check("k_finalize_img attribute");
+      attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = after_stats ? 1 : 0;
+    cfg.gridDim = dim3(std::min(batch, sm_count()), 1, 1);
+    cfg.blockDim = dim3(kImgThreads, 1, 1);
+    cfg.dynamicSmemBytes = kImgSmemBytes;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FinParams fc = f;
+    fc.b_base = 0;
+    const cudaError_t e = f.n_cls > 0 ? cudaLaunchKernelEx(&cfg, k_finalize_img<true>, fc)
+                                      : cudaLaunchKernelEx(&cfg, k_finalize_img<false>, fc);
+    if (e != cudaSuccess) return fail(FV_ERR_CUDA, "k_finalize_img launch: %s", cudaGetErrorString(e));
+    g_launches += 1;
+    return cuda_check("k_finalize_img");
+  }
   if (!after_stats && cudaMemsetAsync(f.counters, 0, (size_t)batch * 4, st) != cudaSuccess)
     return cuda_check("memset tickets");
   for (int b0 = 0; b0 < batch; b0 += 65535) {  // gridDim.y limit

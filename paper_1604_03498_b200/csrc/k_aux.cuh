@@ -272,31 +272,15 @@ __device__ __forceinline__ void slot_sums(const FinParams &p, int b, int j, int 
   }
 }
 
-// grid (ceil(K/32), batch), 256 threads.  Thread (jq = tid % 8, kr = tid / 8) owns Gaussians
-// j0 + 4 jq .. +3 and dims kr, kr + 32: every slot / coefficient read is a 16-byte vector, coalesced
-// over jq (the slots are feature-major rows of Kp Gaussians); U/V go through a shared-memory tile so
-// the global stores are coalesced over (j, k).  The Eq. (6)-(7) combination runs in fp64; the signed
-// square root (P:449, reading A9) in fp32 on the rounded value.  The L2 norm is accumulated with one
-// atomic per block and the LAST block of each image (ticket) rescales it.
-// Fused linear scoring (NEXT-4, P:563-564): each block also writes the dot products of its (pre-L2)
-// U/V tile with the n_cls classifier rows into its own partial slot; the last block sums the slots in
-// block order, divides by the image's norm and adds the bias (bitwise repeatable, no atomics).  With
-// out == nullptr only the scores leave the kernel (the FV is never written to HBM).
 constexpr int kFinKR = 2;  // dims per thread (kr, kr + 32)
-// kSync (small launches, all blocks co-resident: the host uses it when the grid fits in one wave):
-// every block of an image publishes its partial sum of squares, waits for its siblings and writes its
-// tile once, already scaled — no serial rescale of the whole image by its last block (the latency
-// path).  For large batches the last-block variant wins (waiting blocks would hold slots).
-template <bool kScore, bool kSync>  // kScore = false: the plain encode (no scoring code compiled in)
-__global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
-  ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
-  __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
-  __shared__ double s_red[8];
-  __shared__ float s_dot[8][kMaxCls];
-  __shared__ int s_last;
-  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, jq = tid & 7, kr = (tid >> 3) + kDP * (int)blockIdx.z;
-  const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
-  const int kb = kDP * (int)blockIdx.z, nk = min(kDP, p.D - kb);  // this block's dims [kb, kb + nk)
+
+// a6 + a7 for one (32 Gaussians x 64 dims) tile of image b, computed by 256 threads (thread tid:
+// Gaussians j0 + 4 jq .. +3, dims kr, kr + 32): U/V after the signed square root (or raw, mode 2) into
+// sU/sV[j - j0][k - kb]; returns this thread's share of the squared norm (sum |U| + |V|).
+__device__ __forceinline__ double fin_tile(const FinParams &p, int b, int j0, int kb, int tid, float (*sU)[kDP + 1],
+                                           float (*sV)[kDP + 1]) {
+  const int jq = tid & 7, kr = (tid >> 3) + kb;
+  const int nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
   const int KD = p.K * p.D;
   double ss = 0.0;
   if (4 * jq < nj) {
@@ -434,6 +418,35 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
       }
     }
   }
+  return ss;
+}
+
+// grid (ceil(K/32), batch), 256 threads.  Thread (jq = tid % 8, kr = tid / 8) owns Gaussians
+// j0 + 4 jq .. +3 and dims kr, kr + 32: every slot / coefficient read is a 16-byte vector, coalesced
+// over jq (the slots are feature-major rows of Kp Gaussians); U/V go through a shared-memory tile so
+// the global stores are coalesced over (j, k).  The Eq. (6)-(7) combination runs in fp64; the signed
+// square root (P:449, reading A9) in fp32 on the rounded value.  The L2 norm is accumulated with one
+// atomic per block and the LAST block of each image (ticket) rescales it.
+// Fused linear scoring (NEXT-4, P:563-564): each block also writes the dot products of its (pre-L2)
+// U/V tile with the n_cls classifier rows into its own partial slot; the last block sums the slots in
+// block order, divides by the image's norm and adds the bias (bitwise repeatable, no atomics).  With
+// out == nullptr only the scores leave the kernel (the FV is never written to HBM).
+// kSync (small launches, all blocks co-resident: the host uses it when the grid fits in one wave):
+// every block of an image publishes its partial sum of squares, waits for its siblings and writes its
+// tile once, already scaled — no serial rescale of the whole image by its last block (the latency
+// path).  For large batches the last-block variant wins (waiting blocks would hold slots).
+template <bool kScore, bool kSync>  // kScore = false: the plain encode (no scoring code compiled in)
+__global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
+  ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
+  __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
+  __shared__ double s_red[8];
+  __shared__ float s_dot[8][kMaxCls];
+  __shared__ int s_last;
+  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x;
+  const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0);
+  const int kb = kDP * (int)blockIdx.z, nk = min(kDP, p.D - kb);  // this block's dims [kb, kb + nk)
+  const int KD = p.K * p.D;
+  double ss = fin_tile(p, b, j0, kb, tid, sU, sV);
   __syncthreads();
   const int part = blockIdx.z * gridDim.x + blockIdx.x, nparts = gridDim.x * gridDim.z;
   if (!kSync && (!kScore || p.out)) {
@@ -564,6 +577,68 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
       const int t = t0 + u * 256 + tid;
       if (t < n4) { v[u].x *= sc; v[u].y *= sc; v[u].z *= sc; v[u].w *= sc; ob[t] = v[u]; }
     }
+  }
+}
+
+// Whole-image finalize for large batches (D <= 64, K <= 256): persistent blocks of 512 threads take
+// whole images; the two 256-thread groups compute the image's (32 x 64) tiles with fin_tile into a
+// shared-memory copy of the image (2 x 256 x 65 floats), the block reduces the squared norm in a fixed
+// order and writes the FV exactly once, already scaled — no per-image atomics, no last-block re-read
+// of the image.  Scores (kScore) are taken from the same shared-memory image.
+constexpr int kImgK = 256;
+constexpr int kImgThreads = 512;
+constexpr int kImgSmemBytes = 2 * kImgK * (kDP + 1) * 4;
+template <bool kScore>
+__global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams p) {
+  ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
+  extern __shared__ float fimg[];
+  float(*iU)[kDP + 1] = reinterpret_cast<float(*)[kDP + 1]>(fimg);
+  float(*iV)[kDP + 1] = reinterpret_cast<float(*)[kDP + 1]>(fimg + kImgK * (kDP + 1));
+  __shared__ double s_red[kImgThreads / 32];
+  __shared__ float s_dot[kImgThreads / 32][kMaxCls];
+  const int tid = threadIdx.x, grp = tid >> 8, gt = tid & 255, lane = tid & 31, warp = tid >> 5;
+  const int KD = p.K * p.D, ntiles = (p.K + kFinJ - 1) / kFinJ;
+  const bool l2 = p.mode != 2;
+  for (int b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    double ss = 0.0;
+    for (int t = grp; t < ntiles; t += kImgThreads / 256) ss += fin_tile(p, b, t * kFinJ, 0, gt, iU + t * kFinJ, iV + t * kFinJ);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if (lane == 0) s_red[warp] = ss;
+    __syncthreads();
+    double n2 = 0.0;  // fixed order: bitwise repeatable
+    for (int w = 0; w < kImgThreads / 32; ++w) n2 += s_red[w];
+    const float sc = (l2 && n2 > 0.0) ? (float)(1.0 / sqrt(n2)) : 1.f;
+    if (kScore) {
+      for (int c = 0; c < p.n_cls; ++c) {
+        const float *wc = p.svm_w + (size_t)c * 2 * KD;
+        float a = 0.f;
+        for (int e = tid; e < KD; e += kImgThreads) {
+          const int j = e / p.D, k = e - j * p.D;
+          a = fmaf(iU[j][k], __ldg(wc + e), a);
+          a = fmaf(iV[j][k], __ldg(wc + KD + e), a);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+        if (lane == 0) s_dot[warp][c] = a;
+      }
+      __syncthreads();
+      if (tid < p.n_cls) {
+        double d = 0.0;
+        for (int w = 0; w < kImgThreads / 32; ++w) d += (double)s_dot[w][tid];
+        const double inv = l2 ? (n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0) : 1.0;
+        p.scores[(size_t)b * p.n_cls + tid] = (float)(d * inv + (p.svm_b ? (double)p.svm_b[tid] : 0.0));
+      }
+    }
+    if (!kScore || p.out) {
+      float *o = p.out + (size_t)b * 2 * KD;
+      for (int e = tid; e < KD; e += kImgThreads) {
+        const int j = e / p.D, k = e - j * p.D;
+        o[e] = iU[j][k] * sc;
+        o[KD + e] = iV[j][k] * sc;
+      }
+    }
+    __syncthreads();  // the next image overwrites the shared image and s_red
   }
 }
 
