@@ -6,7 +6,9 @@ imports it, and it never imports the product package.  See oracle/fv_oracle.c fo
 the PAPER.md passages each function follows.
 
 Parity status: every function here is pinned by tests/test_oracle.py (closed forms, invariants,
-mpmath brute force); none is "parity unpinned".
+mpmath brute force, scipy / numpy library routines); none is "parity unpinned".  The §8(f) rows are
+plain numpy in oracle/oracle.py: ``score`` (NEXT-4, linear decision values), ``loglik_rows`` /
+``em_step`` (NEXT-3, diagonal-GMM EM with SPEC's floors), ``embed`` (NEXT-2, PCA + normalised xy).
 """
 from .oracle import (  # noqa: F401
     NORM_IMPROVED,
