@@ -109,6 +109,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
   const int64_t T = p.tile_start[p.batch];
   const int t0 = (int)((int64_t)cid * T / ncl), t1 = (int)((int64_t)(cid + 1) * T / ncl);
   const int n = t1 - t0;
+  // D <= 96 (e.g. the paper's 82-dim descriptors): dims 96..127 are padding — box 3 is neither loaded
+  // nor converted (its Zr columns are zeroed once) and GEMM1 skips half b's k-steps 2, 3, 6, 7
+  const bool skip3 = !kD128 && p.D <= 96;
 
   if (warp == kWarpTma) {
     // ======================================================= tile walk + X producer (TMA)
@@ -136,6 +139,10 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         for (int bx = 0; bx < 4; ++bx) {
           const int st = bx & 1;
           if (i >= 1 || bx >= 2) mbar_wait(&bars[W_XEMPTY0 + st], ((bx >> 1) + 1) & 1);
+          if (bx == 3 && skip3) {  // D <= 96: box 3 is all padding; keep the stage's phase sequence
+            mbar_arrive(&bars[W_XFULL0 + st]);
+            continue;
+          }
           mbar_arrive_expect_tx(&bars[W_XFULL0 + st], kXBoxBytes);
           tma_load_2d(sX + st * kXBoxBytes, &tmap_x, 32 * bx, m.row0, &bars[W_XFULL0 + st]);
         }
@@ -155,8 +162,10 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         const uint32_t za = tmem + kWTZr + 128 * hf + (s == 1 ? 64 : 0);           // hi, lo, hi
         const uint32_t wb = sW + hf * (kWImgBytes / 2) + (s == 0 ? kGW * 128 * 2 : 0);  // lo, hi, hi
         const bool first = (s == 0 && hf == 0);
+        const uint32_t mask = (hf == 1 && skip3) ? 0x33u : 0xFFu;  // k-steps holding dims < 96
 #pragma unroll
         for (int kk = 0; kk < kNF / 16; ++kk) {
+          if (!((mask >> kk) & 1u)) continue;
           const uint32_t off = (kk >> 2) * (kGW * 128) + (kk & 3) * 32;
           mma_f16_ts(tmem + kWTL, za + kk * 8, desc_sw128(wb + off, 16, 1024), idesc1, (first && kk == 0) ? 0u : 1u);
         }
@@ -231,7 +240,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         // the tile's metadata is published before its first box: read it only after a box wait
         const int nrows = s_meta[i & 3].nrows;
         const uint8_t *xbox = smem + kWX + st * kXBoxBytes;
-        if (!kD128 || nrows < kTileM)
+        if (bx == 3 && skip3) {
+        } else if (!kD128 || nrows < kTileM)
           zr_box<true>(xbox, row, bl, h, p.D - kDP * hf, row < nrows, s_sc + kDP * hf, s_ncs + kDP * hf, ta);
         else
           zr_box<false>(xbox, row, bl, h, kDP, true, s_sc + kDP * hf, s_ncs + kDP * hf, ta);
@@ -295,6 +305,11 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
     for (int j = 0; j < 16; ++j) s0acc[j] = 0.f;
     int prev_b = 0;
     bool prev_fold = false, chunk_seg_first = true;
+    if (n > 0 && skip3) {  // the Zr columns of dims 96..127 (box 3 of half b) stay zero for the whole run
+      const uint32_t zero4[4] = {0u, 0u, 0u, 0u};
+      const uint32_t ta = tmem + kWTZr + 128 + lane_base + 16 + 4 * h;
+      tmem_st4(ta, zero4); tmem_st4(ta + 32, zero4); tmem_st4(ta + 64, zero4); tmem_st4(ta + 96, zero4);
+    }
     if (n > 0) { conv_half(0, 0); conv_half(0, 1); }
     for (int i = 0; i < n; ++i) {
       TRW(0);
