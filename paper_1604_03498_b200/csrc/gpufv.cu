@@ -1,6 +1,9 @@
 // gpufv.cu — host side of the C ABI declared in include/gpufv.h: argument validation, workspace
 // layout, launches.  No allocation, no synchronisation (except fv_encode_batched_host, which must
 // return host results), no CPU fallback: every step of the path runs in the kernels below.
+// Experiment knobs (environment, read once per process; defaults are the measured best):
+//   GPUFV_MIN_TILES=<n>   minimum tiles per cluster for small launches (default 4)
+//   GPUFV_FIN_TILES=1     force the tile-parallel finalize for large batches (default: k_finalize_img)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -352,14 +355,20 @@ fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStrea
   if (batch == 0) return FV_OK;
   // large batches of narrow images: one persistent block per SM takes whole images (k_finalize_img)
   if (D <= kDP && K <= kImgK && batch >= 2 * sm_count() && !std::getenv("GPUFV_FIN_TILES")) {
-    static bool attr_done = false;
-    if (!attr_done) {
-      if (cudaFuncSetAttribute(k_finalize_img<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgSmemBytes) !=
-              cudaSuccess ||
-          cudaFuncSetAttribute(k_finalize_img<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgSmemBytes) !=
-              cudaSuccess)
-        return cuda_check("k_finalize_img attribute");
-      attr_done = true;
+    static std::mutex mu;
+    static bool attr_done[64] = {};  // the attribute is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (dev < 0 || dev >= 64 || !attr_done[dev]) {
+        if (cudaFuncSetAttribute(k_finalize_img<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgSmemBytes) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_finalize_img<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgSmemBytes) !=
+                cudaSuccess)
+          return cuda_check("k_finalize_img attribute");
+        if (dev >= 0 && dev < 64) attr_done[dev] = true;
+      }
     }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
