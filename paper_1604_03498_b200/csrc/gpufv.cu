@@ -354,7 +354,8 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
 fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStream_t st, bool after_stats = true) {
   if (batch == 0) return FV_OK;
   // large batches of narrow images: one persistent block per SM takes whole images (k_finalize_img)
-  if (D <= kDP && K <= kImgK && batch >= 2 * sm_count() && !std::getenv("GPUFV_FIN_TILES")) {
+  static const bool force_tiles = std::getenv("GPUFV_FIN_TILES") != nullptr;
+  if (D <= kDP && K <= kImgK && batch >= 2 * sm_count() && !force_tiles) {
     static std::mutex mu;
     static bool attr_done[64] = {};  // the attribute is per device
     int dev = 0;
