@@ -17,7 +17,9 @@ using namespace gpufv::ptx;
 constexpr int kThreads = 576, kWork = 16;
 constexpr int kSmem = 200 * 1024;
 
-// mode bits: 1 = MMA TS, 2 = MMA SS, 4 = WORK tcgen05.st, 8 = WORK tcgen05.ld, 16 = WORK st.shared
+// mode bits: 1 = MMA TS, 2 = MMA SS, 4 = WORK tcgen05.st, 8 = WORK tcgen05.ld, 16 = WORK st.shared,
+// 32 = WORK fp32 -> fp16x2 split (cvt.rn.f16x2.f32 + unpack + fadd2 + cvt: the P / feature split),
+// 64 = WORK ex2.approx (MUFU)
 __global__ void __launch_bounds__(kThreads, 1) probe(int mode, int iters, long long *out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t s_tmem;
@@ -68,6 +70,28 @@ __global__ void __launch_bounds__(kThreads, 1) probe(int mode, int iters, long l
 #pragma unroll
         for (int j = 0; j < 8; ++j) sts128(sbase + 131072 + ((warp * 8 + j) * 32 + lane) * 16 % 65536, r[j], r[j + 1], r[j + 2], r[j + 3]);
     }
+    if (mode & 32) {
+      float2 a = make_float2(__uint_as_float(r[0]) * 1e-30f + 0.37f, __uint_as_float(r[1]) * 1e-30f + 0.61f);
+      uint32_t acc = 0;
+      for (int it = 0; it < witers * 8; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t hi, lo;
+          split2_f16(a, hi, lo);
+          acc ^= hi + lo;
+          a.x += 1e-3f; a.y -= 1e-3f;
+        }
+      }
+      r[0] = acc;
+    }
+    if (mode & 64) {
+      float x = __uint_as_float(r[0]) * 1e-30f;
+      for (int it = 0; it < witers * 8; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x = ex2_approx(x) * -0.5f;
+      }
+      r[0] = __float_as_uint(x);
+    }
     if (r[0] == 0xdeadbeef) out[1] = r[1];
     if (blockIdx.x == 0 && lane == 0) atomicMax(reinterpret_cast<unsigned long long *>(out + 3), (unsigned long long)(clock64() - t0));
   }
@@ -87,7 +111,7 @@ int main() {
       {1, "TS MMA alone"}, {2, "SS MMA alone"}, {4, "tcgen05.st alone"}, {8, "tcgen05.ld alone"},
       {16, "st.shared alone"}, {1 | 4, "TS MMA + tcgen05.st"}, {1 | 8, "TS MMA + tcgen05.ld"},
       {1 | 16, "TS MMA + st.shared"}, {2 | 4, "SS MMA + tcgen05.st"}, {2 | 16, "SS MMA + st.shared"},
-      {2 | 8, "SS MMA + tcgen05.ld"}};
+      {2 | 8, "SS MMA + tcgen05.ld"}, {32, "fp16x2 split alone"}, {64, "ex2 alone"}, {1 | 32, "TS MMA + split"}};
   for (auto &c : cases) {
     probe<<<148, kThreads, kSmem>>>(c.mode, iters, d);  // warm-up
     cudaMemset(d, 0, 64);
@@ -98,10 +122,14 @@ int main() {
     const double mma = (c.mode & 3) ? (double)iters * 8 : 0;
     const double wbytes = (c.mode & 4 || c.mode & 8) ? (double)iters * 2 * 16 * 32 * 32 * 4 : 0;  // per warp 4 KB per op
     const double sbytes = (c.mode & 16) ? (double)iters * 2 * 16 * 8 * 512 : 0;
+    const double nsplit = (c.mode & 32) ? (double)iters * 2 * 8 * 8 * 16 * 32 : 0;  // pairs split per SM
+    const double nex2 = (c.mode & 64) ? (double)iters * 2 * 8 * 8 * 16 * 32 : 0;
     printf("%-24s %10lld cycles (mma %lld, work %lld)", c.name, cyc, cmma, cwork);
     if (mma) printf("  %6.1f cyc/UMMA", cmma / mma);
     if (wbytes) printf("  TMEM %6.1f B/clk", wbytes / cwork);
     if (sbytes) printf("  SMEM st %6.1f B/clk", sbytes / cwork);
+    if (nsplit) printf("  split %6.2f pairs/clk", nsplit / cwork);
+    if (nex2) printf("  ex2 %6.2f /clk", nex2 / cwork);
     printf("\n");
   }
   return 0;
