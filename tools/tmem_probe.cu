@@ -19,7 +19,8 @@ constexpr int kSmem = 200 * 1024;
 
 // mode bits: 1 = MMA TS, 2 = MMA SS, 4 = WORK tcgen05.st, 8 = WORK tcgen05.ld, 16 = WORK st.shared,
 // 32 = WORK fp32 -> fp16x2 split (cvt.rn.f16x2.f32 + unpack + fadd2 + cvt: the P / feature split),
-// 64 = WORK ex2.approx (MUFU)
+// 64 = WORK ex2.approx (MUFU), 128 = split with the hi part rounded by integer ops (no unpack),
+// 256 = only the WORK warps NOT on the MMA warp's sub-partition (warp % 4 != 0) do the WORK traffic
 __global__ void __launch_bounds__(kThreads, 1) probe(int mode, int iters, long long *out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t s_tmem;
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(kThreads, 1) probe(int mode, int iters, long l
       mbar_wait(&bar, 0);
       if (blockIdx.x == 0) out[2] = clock64() - t0;  // MMA stream done
     }
-  } else if (warp < kWork) {
+  } else if (warp < kWork && !((mode & 256) && (warp & 3) == 0)) {
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     uint32_t r[32];
 #pragma unroll
@@ -84,6 +85,23 @@ __global__ void __launch_bounds__(kThreads, 1) probe(int mode, int iters, long l
       }
       r[0] = acc;
     }
+    if (mode & 128) {
+      float2 a = make_float2(__uint_as_float(r[0]) * 1e-30f + 0.37f, __uint_as_float(r[1]) * 1e-30f + 0.61f);
+      uint32_t acc = 0;
+      for (int it = 0; it < witers * 8; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 hf = make_float2(__uint_as_float((__float_as_uint(a.x) + 0x1000u) & 0xFFFFE000u),
+                                        __uint_as_float((__float_as_uint(a.y) + 0x1000u) & 0xFFFFE000u));
+          const __half2 h = __floats2half2_rn(hf.x, hf.y);
+          const float2 d = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
+          const __half2 l = __floats2half2_rn(d.x, d.y);
+          acc ^= *reinterpret_cast<const uint32_t *>(&h) + *reinterpret_cast<const uint32_t *>(&l);
+          a.x += 1e-3f; a.y -= 1e-3f;
+        }
+      }
+      r[0] = acc;
+    }
     if (mode & 64) {
       float x = __uint_as_float(r[0]) * 1e-30f;
       for (int it = 0; it < witers * 8; ++it) {
@@ -111,7 +129,9 @@ int main() {
       {1, "TS MMA alone"}, {2, "SS MMA alone"}, {4, "tcgen05.st alone"}, {8, "tcgen05.ld alone"},
       {16, "st.shared alone"}, {1 | 4, "TS MMA + tcgen05.st"}, {1 | 8, "TS MMA + tcgen05.ld"},
       {1 | 16, "TS MMA + st.shared"}, {2 | 4, "SS MMA + tcgen05.st"}, {2 | 16, "SS MMA + st.shared"},
-      {2 | 8, "SS MMA + tcgen05.ld"}, {32, "fp16x2 split alone"}, {64, "ex2 alone"}, {1 | 32, "TS MMA + split"}};
+      {2 | 8, "SS MMA + tcgen05.ld"}, {32, "fp16x2 split alone"}, {64, "ex2 alone"}, {1 | 32, "TS MMA + split"}, {128, "int-round split alone"},
+      {1 | 128, "TS MMA + int-round split"}, {1 | 32 | 256, "TS MMA + split (not SMSP0)"},
+      {1 | 128 | 256, "TS MMA + int split (not SMSP0)"}, {2 | 32, "SS MMA + split"}, {2 | 32 | 256, "SS MMA + split (not SMSP0)"}};
   for (auto &c : cases) {
     probe<<<148, kThreads, kSmem>>>(c.mode, iters, d);  // warm-up
     cudaMemset(d, 0, 64);
@@ -122,7 +142,7 @@ int main() {
     const double mma = (c.mode & 3) ? (double)iters * 8 : 0;
     const double wbytes = (c.mode & 4 || c.mode & 8) ? (double)iters * 2 * 16 * 32 * 32 * 4 : 0;  // per warp 4 KB per op
     const double sbytes = (c.mode & 16) ? (double)iters * 2 * 16 * 8 * 512 : 0;
-    const double nsplit = (c.mode & 32) ? (double)iters * 2 * 8 * 8 * 16 * 32 : 0;  // pairs split per SM
+    const double nsplit = (c.mode & (32 | 128)) ? (double)iters * 2 * 8 * 8 * 16 * 32 : 0;  // pairs split per SM
     const double nex2 = (c.mode & 64) ? (double)iters * 2 * 8 * 8 * 16 * 32 : 0;
     printf("%-24s %10lld cycles (mma %lld, work %lld)", c.name, cyc, cmma, cwork);
     if (mma) printf("  %6.1f cyc/UMMA", cmma / mma);
