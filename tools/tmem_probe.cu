@@ -20,7 +20,8 @@ constexpr int kSmem = 200 * 1024;
 // mode bits: 1 = MMA TS, 2 = MMA SS, 4 = WORK tcgen05.st, 8 = WORK tcgen05.ld, 16 = WORK st.shared,
 // 32 = WORK fp32 -> fp16x2 split (cvt.rn.f16x2.f32 + unpack + fadd2 + cvt: the P / feature split),
 // 64 = WORK ex2.approx (MUFU), 128 = split with the hi part rounded by integer ops (no unpack),
-// 256 = only the WORK warps NOT on the MMA warp's sub-partition (warp % 4 != 0) do the WORK traffic
+// 256 = only the WORK warps NOT on the MMA warp's sub-partition (warp % 4 != 0) do the WORK traffic,
+// 512 = split with the hi part from a Veltkamp split on the FMA pipe (c = a (2^13 + 1), hi = c - (c - a))
 __global__ void __launch_bounds__(kThreads, 1) probe(int mode, int iters, long long *out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t s_tmem;
@@ -102,6 +103,24 @@ __global__ void __launch_bounds__(kThreads, 1) probe(int mode, int iters, long l
       }
       r[0] = acc;
     }
+    if (mode & 512) {
+      float2 a = make_float2(__uint_as_float(r[0]) * 1e-30f + 0.37f, __uint_as_float(r[1]) * 1e-30f + 0.61f);
+      uint32_t acc = 0;
+      const float2 kSplit = make_float2(8193.f, 8193.f);
+      for (int it = 0; it < witers * 8; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 c = __fmul2_rn(a, kSplit);
+          const float2 hf = __fadd2_rn(c, __fadd2_rn(a, make_float2(-c.x, -c.y)));
+          const __half2 h = __floats2half2_rn(hf.x, hf.y);
+          const float2 d = __fadd2_rn(a, make_float2(-hf.x, -hf.y));
+          const __half2 l = __floats2half2_rn(d.x, d.y);
+          acc ^= *reinterpret_cast<const uint32_t *>(&h) + *reinterpret_cast<const uint32_t *>(&l);
+          a.x += 1e-3f; a.y -= 1e-3f;
+        }
+      }
+      r[0] = acc;
+    }
     if (mode & 64) {
       float x = __uint_as_float(r[0]) * 1e-30f;
       for (int it = 0; it < witers * 8; ++it) {
@@ -131,7 +150,8 @@ int main() {
       {1 | 16, "TS MMA + st.shared"}, {2 | 4, "SS MMA + tcgen05.st"}, {2 | 16, "SS MMA + st.shared"},
       {2 | 8, "SS MMA + tcgen05.ld"}, {32, "fp16x2 split alone"}, {64, "ex2 alone"}, {1 | 32, "TS MMA + split"}, {128, "int-round split alone"},
       {1 | 128, "TS MMA + int-round split"}, {1 | 32 | 256, "TS MMA + split (not SMSP0)"},
-      {1 | 128 | 256, "TS MMA + int split (not SMSP0)"}, {2 | 32, "SS MMA + split"}, {2 | 32 | 256, "SS MMA + split (not SMSP0)"}};
+      {1 | 128 | 256, "TS MMA + int split (not SMSP0)"}, {2 | 32, "SS MMA + split"}, {2 | 32 | 256, "SS MMA + split (not SMSP0)"},
+      {512, "Veltkamp split alone"}, {1 | 512, "TS MMA + Veltkamp split"}};
   for (auto &c : cases) {
     probe<<<148, kThreads, kSmem>>>(c.mode, iters, d);  // warm-up
     cudaMemset(d, 0, 64);
@@ -142,7 +162,7 @@ int main() {
     const double mma = (c.mode & 3) ? (double)iters * 8 : 0;
     const double wbytes = (c.mode & 4 || c.mode & 8) ? (double)iters * 2 * 16 * 32 * 32 * 4 : 0;  // per warp 4 KB per op
     const double sbytes = (c.mode & 16) ? (double)iters * 2 * 16 * 8 * 512 : 0;
-    const double nsplit = (c.mode & (32 | 128)) ? (double)iters * 2 * 8 * 8 * 16 * 32 : 0;  // pairs split per SM
+    const double nsplit = (c.mode & (32 | 128 | 512)) ? (double)iters * 2 * 8 * 8 * 16 * 32 : 0;  // pairs split per SM
     const double nex2 = (c.mode & 64) ? (double)iters * 2 * 8 * 8 * 16 * 32 : 0;
     printf("%-24s %10lld cycles (mma %lld, work %lld)", c.name, cyc, cmma, cwork);
     if (mma) printf("  %6.1f cyc/UMMA", cmma / mma);
