@@ -1,0 +1,53 @@
+"""Randomised GPU parity sweep (seeded, reproducible): many (K, D, image-size mix, tau, normalisation,
+sigma convention) combinations across both tile families, each against the fp64 oracle with the
+north_star tolerances (FV 1e-4 relative L2; empty images all-zero; every FV finite).  Complements the
+hand-picked cases in test_gpu_parity.py / test_gpu_wide.py with shapes nobody chose on purpose."""
+import numpy as np
+import pytest
+import torch
+
+import fvgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fv():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1604_03498_b200 as m
+    return m
+
+
+def _case(seed):
+    rng = np.random.default_rng(seed)
+    K = int(rng.choice([1, 2, 7, 16, 31, 64, 100, 128, 129, 200, 255, 256, 257, 384, 511, 512]))
+    D = int(4 * rng.integers(1, 33))                      # 4 .. 128, multiples of 4
+    counts = [int(c) for c in rng.choice([0, 1, 17, 127, 128, 129, 300, 1000, 2500], size=int(rng.integers(1, 5)))]
+    if sum(counts) == 0:
+        counts[0] = 64
+    tau = float(rng.choice([0.0, 1e-6, 1e-3]))
+    mode = int(rng.choice([0, 1, 2]))
+    stddev = bool(rng.integers(0, 2))
+    return K, D, counts, tau, mode, stddev
+
+
+@pytest.mark.parametrize("seed", list(range(64)))
+def test_random_shapes_match_oracle(fv, seed):
+    K, D, counts, tau, mode, stddev = _case(7000 + seed)
+    pi, mu, var = fvgen.make_gmm(K, D, seed=7100 + seed)
+    X, off = fvgen.make_batch((pi, mu, var), counts, seed_base=7200 + 10 * seed)
+    sg = np.sqrt(var).astype(np.float32) if stddev else var
+    gmm = fv.GMM(pi, mu, sg, stddev=stddev)
+    out = fv.encode_batched(torch.from_numpy(X).cuda(), torch.from_numpy(off).cuda(), gmm, threshold=tau,
+                            mode=mode).cpu().numpy()
+    ref = oracle.encode_batched(X, off, pi, mu, var, threshold=tau, mode=mode)
+    assert np.all(np.isfinite(out))
+    for b, n in enumerate(counts):
+        if n == 0:
+            assert np.all(out[b] == 0), f"empty image {b} not zero"
+            continue
+        nr = np.linalg.norm(ref[b])
+        err = np.linalg.norm(out[b] - ref[b]) / (nr if nr > 0 else 1.0)
+        assert err <= 1e-4, f"K={K} D={D} counts={counts} tau={tau} mode={mode} stddev={stddev} image {b}: {err:.2e}"
