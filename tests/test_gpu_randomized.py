@@ -51,3 +51,42 @@ def test_random_shapes_match_oracle(fv, seed):
         nr = np.linalg.norm(ref[b])
         err = np.linalg.norm(out[b] - ref[b]) / (nr if nr > 0 else 1.0)
         assert err <= 1e-4, f"K={K} D={D} counts={counts} tau={tau} mode={mode} stddev={stddev} image {b}: {err:.2e}"
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_random_stats_shards_and_scores(fv, seed):
+    """Random shapes through the split path (statistics of two descriptor shards summed, then finalize)
+    and the fused scoring, against the oracle on the whole set."""
+    K, D, counts, tau, mode, _ = _case(8000 + seed)
+    pi, mu, var = fvgen.make_gmm(K, D, seed=8100 + seed)
+    n = max(2, sum(counts))
+    X = fvgen.make_descriptors((pi, mu, var), n, seed=8200 + seed)
+    gmm = fv.GMM(pi, mu, var)
+    cut = n // 3
+    s = sum(fv.stats_batched(torch.from_numpy(np.ascontiguousarray(part)).cuda(),
+                             torch.tensor([0, part.shape[0]], dtype=torch.int64, device="cuda"), gmm, threshold=tau)
+            for part in (X[:cut], X[cut:]))
+    out = fv.finalize(s, gmm, mode=mode).cpu().numpy()[0]
+    ref = oracle.encode(X, pi, mu, var, threshold=tau, mode=mode)
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) <= 1e-4
+    W = np.random.default_rng(8300 + seed).standard_normal((3, 2 * K * D)).astype(np.float32)
+    sc = fv.encode_scored_batched(torch.from_numpy(X).cuda(), torch.tensor([0, n], dtype=torch.int64, device="cuda"),
+                                  gmm, torch.from_numpy(W).cuda(), threshold=tau, mode=mode).cpu().numpy()[0]
+    sref = oracle.score(ref, W)
+    assert np.all(np.abs(sc - sref) <= 1e-4 * np.linalg.norm(W, axis=1) * np.linalg.norm(ref) + 1e-6)
+
+
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_random_em_steps(fv, seed):
+    """Random GMM sizes: one EM step against the oracle (priors 1e-5, log-likelihood 2e-5 per
+    descriptor)."""
+    rng = np.random.default_rng(9000 + seed)
+    K = int(rng.choice([1, 3, 16, 64, 130, 256, 300]))
+    D = int(4 * rng.integers(1, 33))
+    N = int(rng.choice([500, 2000, 5000]))
+    g = fvgen.make_gmm(K, D, seed=9100 + seed)
+    X = fvgen.make_descriptors(g, N, seed=9200 + seed)
+    new, ll = fv.gmm_em_step(torch.from_numpy(X).cuda(), fv.GMM(*g))
+    pi_r, mu_r, var_r, ll_r = oracle.em_step(X, *g)
+    assert abs(float(ll.item()) - ll_r) <= 2e-5 * N
+    assert np.abs(new.weights.cpu().numpy() - pi_r).max() <= 1e-5
