@@ -28,4 +28,14 @@ for a, b in ev:
     a.record(); fv.encode(X, gmm, threshold=1e-6, ws=ws, prepared=True, out=out); b.record()
 torch.cuda.synchronize()
 us = sorted(1e3 * a.elapsed_time(b) for a, b in ev)
-print(f"N={N}: p50 {us[25]:.1f} us, min {us[0]:.1f} us")
+# the stats kernel alone (library hook brackets each k_stats launch with these events)
+kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+for a, b in kev:
+    a.record(); b.record()
+for a, b in kev:
+    fv.profile_events(a, b)
+    fv.encode(X, gmm, threshold=1e-6, ws=ws, prepared=True, out=out)
+fv.profile_events(None, None)
+torch.cuda.synchronize()
+ks = sorted(1e3 * a.elapsed_time(b) for a, b in kev)
+print(f"N={N}: p50 {us[25]:.1f} us, min {us[0]:.1f} us; k_stats p50 {ks[25]:.1f} us")
