@@ -225,12 +225,14 @@ uint8_t *at(void *ws, size_t off) { return static_cast<uint8_t *>(ws) + off; }
 fv_status launch_prep(const Layout &L, const float *w, const float *mu, const float *sg, int K, int D, unsigned flags,
                       void *ws, cudaStream_t st) {
   const int sd = (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0;
-  k_prep_shift<<<1, 256, 0, st>>>(w, mu, sg, K, D, L.Kp, sd, (double *)at(ws, L.cshift), (float *)at(ws, L.xshift),
-                                  (float *)at(ws, L.xscale), (float *)at(ws, L.bias), (double *)at(ws, L.bscratch),
-                                  (double *)at(ws, L.bmax), (double *)at(ws, L.pscale), (double *)at(ws, L.xinv));
+  k_prep_shift<<<1, kPrepThreads, 0, st>>>(w, mu, sg, K, D, L.Kp, sd, (double *)at(ws, L.cshift), (float *)at(ws, L.xshift),
+                                  (float *)at(ws, L.xscale), (double *)at(ws, L.pscale), (double *)at(ws, L.xinv));
+  k_prep_bias<<<K, kDMax, 0, st>>>(w, mu, sg, D, sd, (const double *)at(ws, L.cshift), (double *)at(ws, L.bscratch));
+  k_prep_bias_final<<<1, 512, 0, st>>>(K, L.Kp, (const double *)at(ws, L.bscratch), (float *)at(ws, L.bias),
+                                       (double *)at(ws, L.bmax));
   k_prep_w<<<L.Kp, 2 * L.dpad, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
                                  at(ws, L.wimg), (double *)at(ws, L.coef), is_wide(K, D) ? 1 : 0);
-  g_launches += 2;
+  g_launches += 4;
   return cuda_check("k_prep");
 }
 

@@ -1,5 +1,6 @@
 // k_aux.cuh — the small kernels around k_stats:
-//   k_prep_shift, k_prep_w   step a1: GMM -> prepared operands (Alg.1 l.1)
+//   k_prep_shift, k_prep_bias, k_prep_bias_final, k_prep_w
+//                            step a1: GMM -> prepared operands (Alg.1 l.1)
 //   k_schedule               tile prefix sums from device offsets (ragged batches)
 //   k_finalize               steps a6 (fixed-order fp64 slot reduction) + a7 (centring, VLFeat
 //                            normalisation, P:449 / reading A9; the last block of each image applies
@@ -20,67 +21,95 @@ __device__ __forceinline__ double gmm_var(const float *sigmas, size_t i, bool st
   return stddev ? s * s : s;
 }
 
-// a1 (part 1): feature shift c_k = sum_j pi_j mu_jk / sum_j pi_j, power-of-two scale 2^e_k with
-// e_k = -E where RMS_k = m 2^E (m in [0.5,1)), and the per-Gaussian bias
-//   b_j = ln pi_j - 1/2 sum_k ln var_jk - 1/2 sum_k (mu_jk - c_k)^2 / var_jk    (minus max_j b_j)
-// in log2 units.  One block of 256 threads.
-__global__ void k_prep_shift(const float *w, const float *mu, const float *sg, int K, int D, int Kp,
-                             int stddev, double *cshift, float *xshift, float *xscale, float *bias,
-                             double *bscratch, double *bmax_out, double *pscale, double *xinv) {
-  __shared__ double s_c[kDMax];
-  __shared__ double s_red[256];
-  const int tid = threadIdx.x;
-  if (tid < kDMax) {
+// a1 (part 1): feature shift c_k = sum_j pi_j mu_jk / sum_j pi_j and power-of-two scale 2^e_k with
+// e_k = -E where RMS_k = m 2^E (m in [0.5,1)), RMS_k^2 = sum_j pi_j (var_jk + mu_jk^2) / sum_j pi_j - c_k^2
+// (one pass, fp64: only the exponent of RMS_k is used); the finalize's prior scales 1/sqrt(pi_j),
+// 1/sqrt(2 pi_j) and inverse feature scales.  One block of 1024 threads: dimension k = tid % dstride
+// (dstride = 64 or 128), Gaussian group tid / dstride, group partials summed in group order.
+constexpr int kPrepThreads = 1024;
+__global__ void __launch_bounds__(kPrepThreads) k_prep_shift(const float *w, const float *mu, const float *sg, int K,
+                                                           int D, int Kp, int stddev, double *cshift, float *xshift,
+                                                           float *xscale, double *pscale, double *xinv) {
+  __shared__ double s_w[kPrepThreads], s_m[kPrepThreads], s_q[kPrepThreads];
+  const int dstride = D <= kDP ? kDP : kDMax, ngrp = kPrepThreads / dstride;
+  const int tid = threadIdx.x, k = tid % dstride, grp = tid / dstride;
+  double ws = 0.0, am = 0.0, aq = 0.0;
+  if (k < D) {
+#pragma unroll 4
+    for (int j = grp; j < K; j += ngrp) {
+      const double wj = (double)w[j], m = (double)mu[(size_t)j * D + k];
+      ws += wj;
+      am += wj * m;
+      aq += wj * (gmm_var(sg, (size_t)j * D + k, stddev) + m * m);
+    }
+  }
+  s_w[tid] = ws; s_m[tid] = am; s_q[tid] = aq;
+  __syncthreads();
+  if (grp == 0) {
+    double W = 0.0, M = 0.0, Q = 0.0;
+    for (int g = 0; g < ngrp; ++g) { W += s_w[g * dstride + k]; M += s_m[g * dstride + k]; Q += s_q[g * dstride + k]; }
     double c = 0.0, sc = 1.0;
-    if (tid < D) {
-      double ws = 0.0, acc = 0.0;
-      for (int j = 0; j < K; ++j) { ws += (double)w[j]; acc += (double)w[j] * (double)mu[(size_t)j * D + tid]; }
-      c = acc / ws;
-      double r = 0.0;
-      for (int j = 0; j < K; ++j) {
-        double d = (double)mu[(size_t)j * D + tid] - c;
-        r += (double)w[j] * (gmm_var(sg, (size_t)j * D + tid, stddev) + d * d);
-      }
-      r = sqrt(r / ws);
+    if (k < D && W > 0.0) {
+      c = M / W;
+      const double r = sqrt(fmax(Q / W - c * c, 0.0));
       int E = 0;
       if (r > 0.0 && isfinite(r)) frexp(r, &E);
       sc = ldexp(1.0, -E);
     }
-    s_c[tid] = c;
-    cshift[tid] = c;
-    xshift[tid] = (float)c;
-    xscale[tid] = (float)sc;
-    xinv[tid] = 1.0 / ((double)kPScale * sc);  // undoes P = gamma 2^14 and the feature scale (exact)
+    cshift[k] = c;
+    xshift[k] = (float)c;
+    xscale[k] = (float)sc;
+    xinv[k] = 1.0 / ((double)kPScale * sc);  // undoes P = gamma 2^14 and the feature scale (exact)
+  }
+  if (tid < kDMax && tid >= dstride) {  // dims past the tile family's width
+    cshift[tid] = 0.0; xshift[tid] = 0.f; xscale[tid] = 1.f; xinv[tid] = 1.0 / (double)kPScale;
   }
   // finalize prior scales of the improved FV (reading A9): 1/sqrt(pi_j), 1/sqrt(2 pi_j)
-  for (int j = tid; j < Kp; j += 256) {
+  for (int j = tid; j < Kp; j += kPrepThreads) {
     pscale[j] = j < K ? 1.0 / sqrt((double)w[j]) : 0.0;
     pscale[Kp + j] = j < K ? 1.0 / sqrt(2.0 * (double)w[j]) : 0.0;
   }
-  __syncthreads();
-  double bmax = -1e300;
-  for (int j = tid; j < K; j += 256) {
-    double ld = 0.0, q = 0.0;
-    for (int k = 0; k < D; ++k) {
-      double v = gmm_var(sg, (size_t)j * D + k, stddev);
-      double d = (double)mu[(size_t)j * D + k] - s_c[k];
-      ld += log(v);
-      q += d * d / v;
-    }
-    double bj = log((double)w[j]) - 0.5 * ld - 0.5 * q;
-    bscratch[j] = bj;
-    bmax = fmax(bmax, bj);
+}
+
+// a1 (part 1b): per-Gaussian bias  b_j = ln pi_j - 1/2 sum_k ln var_jk - 1/2 sum_k (mu_jk - c_k)^2 / var_jk
+// (natural log; the -D/2 ln 2pi constant is dropped, reading A2).  One block of 128 threads per
+// Gaussian, one dimension per thread, fixed-order tree reduction.
+__global__ void __launch_bounds__(kDMax) k_prep_bias(const float *w, const float *mu, const float *sg, int D,
+                                                     int stddev, const double *cshift, double *bscratch) {
+  __shared__ double s_red[kDMax];
+  const int j = blockIdx.x, k = threadIdx.x;
+  double t = 0.0;
+  if (k < D) {
+    const double v = gmm_var(sg, (size_t)j * D + k, stddev);
+    const double d = (double)mu[(size_t)j * D + k] - cshift[k];
+    t = log(v) + d * d / v;
   }
+  s_red[k] = t;
+  __syncthreads();
+  for (int o = kDMax / 2; o > 0; o >>= 1) {
+    if (k < o) s_red[k] += s_red[k + o];
+    __syncthreads();
+  }
+  if (k == 0) bscratch[j] = log((double)w[j]) - 0.5 * s_red[0];
+}
+
+// a1 (part 1c): bias shift bmax = max_j b_j and the kernel's bias (b_j - bmax) log2 e (padded
+// Gaussians: -1e30).  One block of 512 threads.
+__global__ void __launch_bounds__(512) k_prep_bias_final(int K, int Kp, const double *bscratch, float *bias,
+                                                         double *bmax_out) {
+  __shared__ double s_red[512];
+  const int tid = threadIdx.x;
+  double bmax = -1e300;
+  for (int j = tid; j < K; j += 512) bmax = fmax(bmax, bscratch[j]);
   s_red[tid] = bmax;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
+  for (int o = 256; o > 0; o >>= 1) {
     if (tid < o) s_red[tid] = fmax(s_red[tid], s_red[tid + o]);
     __syncthreads();
   }
   bmax = s_red[0];
   if (tid == 0) *bmax_out = bmax;  // the bias shift (natural log units): log-likelihoods add it back
-  for (int j = tid; j < Kp; j += 256)
-    bias[j] = (j < K) ? (float)((bscratch[j] - bmax) * kLog2e) : -1.0e30f;
+  for (int j = tid; j < Kp; j += 512) bias[j] = (j < K) ? (float)((bscratch[j] - bmax) * kLog2e) : -1.0e30f;
 }
 
 // a1 (part 2): W'_jf (log2 units, scaled by the feature exponents) split into fp16 hi/lo and stored

@@ -38,4 +38,10 @@ for a, b in kev:
 fv.profile_events(None, None)
 torch.cuda.synchronize()
 ks = sorted(1e3 * a.elapsed_time(b) for a, b in kev)
-print(f"N={N}: p50 {us[25]:.1f} us, min {us[0]:.1f} us; k_stats p50 {ks[25]:.1f} us")
+# without FV_PREPARED: the GMM preparation (step a1) runs inside every call
+ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+for a, b in ev2:
+    a.record(); fv.encode(X, gmm, threshold=1e-6, ws=ws, prepared=False, out=out); b.record()
+torch.cuda.synchronize()
+up = sorted(1e3 * a.elapsed_time(b) for a, b in ev2)
+print(f"N={N}: p50 {us[25]:.1f} us, min {us[0]:.1f} us; k_stats p50 {ks[25]:.1f} us; unprepared call p50 {up[25]:.1f} us")
