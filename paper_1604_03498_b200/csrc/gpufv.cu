@@ -145,7 +145,10 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   // ... and at most ~kMaxSegPerImage segments per image on average: the finalize of one image costs
   // ~1 us per extra segment (measured: one 40,000-descriptor image 157 us over 74 clusters, 92 us
   // over 26), so a single large image uses fewer, longer cluster ranges
-  if (batch > 0) L.ncl = (int)std::min<int64_t>(L.ncl, (int64_t)kMaxSegPerImage * batch);
+  // (only for small images — up to 32 tiles per cluster at the cap; a large single set such as an EM
+  // pass or a descriptor shard needs every cluster)
+  if (batch > 0 && tmax <= (int64_t)kMaxSegPerImage * 32 * batch)
+    L.ncl = (int)std::min<int64_t>(L.ncl, (int64_t)kMaxSegPerImage * batch);
   // one slot per (cluster, image) segment, index cid + b (seg_slot, fv_common.cuh)
   L.n_total = n_total;
   L.nslots = (int64_t)L.ncl + batch + 1;

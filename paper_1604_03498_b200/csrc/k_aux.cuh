@@ -739,16 +739,28 @@ __global__ void __launch_bounds__(1024) k_mstep(const double *st, int K, int D, 
                                                 float *var_new) {
   __shared__ double s_floor[kDMax];
   __shared__ double s_red[32];
+  __shared__ double s_a[1024], s_b[1024];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double N = st[0];
   const double *S0 = st + 1, *S1 = st + 1 + K, *S2 = st + 1 + K + (size_t)K * D;
   (void)w_old;
-  if (tid < D) {
+  {  // global per-dimension moments from the statistics: dimension k = tid % dstride, Gaussian groups
+     // tid / dstride (j = group + ngrp i), group partials summed in group order
+    const int dstride = D <= kDP ? kDP : kDMax, ngrp = 1024 / dstride, k = tid % dstride, grp = tid / dstride;
     double a = 0.0, b = 0.0;
-    for (int j = 0; j < K; ++j) { a += S1[(size_t)j * D + tid]; b += S2[(size_t)j * D + tid]; }
-    const double m1 = N > 0.0 ? a / N : 0.0;
-    const double gv = N > 0.0 ? b / N - m1 * m1 : 0.0;
-    s_floor[tid] = fmax(floor_abs, floor_rel * gv);
+    if (k < D) {
+#pragma unroll 4
+      for (int j = grp; j < K; j += ngrp) { a += S1[(size_t)j * D + k]; b += S2[(size_t)j * D + k]; }
+    }
+    s_a[tid] = a; s_b[tid] = b;
+    __syncthreads();
+    if (grp == 0 && k < D) {
+      double A = 0.0, B = 0.0;
+      for (int g = 0; g < ngrp; ++g) { A += s_a[g * dstride + k]; B += s_b[g * dstride + k]; }
+      const double m1 = N > 0.0 ? A / N : 0.0;
+      const double gv = N > 0.0 ? B / N - m1 * m1 : 0.0;
+      s_floor[k] = fmax(floor_abs, floor_rel * gv);
+    }
   }
   double ps = 0.0;
   for (int j = tid; j < K; j += 1024) ps += fmax(N > 0.0 ? S0[j] / N : 0.0, prior_floor);
