@@ -810,6 +810,15 @@ def main():
         except Exception as e:  # noqa: BLE001
             latency["graph_us"] = f"capture failed: {e}"
         latency["workload"] = f"one frame, {PER_FRAME} descriptors, K={K}, D={D}, tau={TAU} (C2)"
+        # C2 at the paper's geometry (8 scales, stride 4 on 320x240 = 17,714 descriptors)
+        n_pg = 17714
+        x_pg = torch.from_numpy(fvgen.make_descriptors(gmm_np, n_pg, seed=1604 + 1000)).to(dev)
+        ws_pg = fv.Workspace(device=dev)
+        ws_pg.ensure(fv.workspace_bytes(n_pg, 1, K, D))
+        fv.gmm_prepare(gmm, ws_pg)
+        latency["paper_geometry_eager_us"] = timed(
+            lambda: fv.encode(x_pg, gmm, threshold=TAU, ws=ws_pg, prepared=True, out=o1))
+        latency["paper_geometry_workload"] = f"one frame, {n_pg} descriptors (paper geometry), K={K}, D={D}, tau={TAU}"
 
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
