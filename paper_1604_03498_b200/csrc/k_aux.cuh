@@ -436,8 +436,8 @@ __device__ __forceinline__ double fin_tile(const FinParams &p, int b, int j0, in
           U = zero ? 0.0 : U * fu[e];
           V = zero ? 0.0 : V * fv[e];
           ss += fabs(U) + fabs(V);  // = (signed sqrt)^2
-          u = copysignf(sqrtf(fabsf((float)U)), (float)U);
-          v = copysignf(sqrtf(fabsf((float)V)), (float)V);
+          u = signed_sqrt((float)U);
+          v = signed_sqrt((float)V);
         } else {
           u = (float)U;
           v = (float)V;
@@ -465,7 +465,7 @@ __device__ __forceinline__ double fin_tile(const FinParams &p, int b, int j0, in
 // tile once, already scaled — no serial rescale of the whole image by its last block (the latency
 // path).  For large batches the last-block variant wins (waiting blocks would hold slots).
 template <bool kScore, bool kSync>  // kScore = false: the plain encode (no scoring code compiled in)
-__global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
+__global__ void __launch_bounds__(256, 2) k_finalize(const FinParams p) {
   ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
   __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
   __shared__ double s_red[8];
@@ -609,6 +609,117 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
   }
 }
 
+// fin_tile for k_finalize_img (slots mode, segment list of the image precomputed): one round of loads
+// per segment pair (S1 and S2 of every thread, S0 of the 4 Gaussians by the 8 threads with kr == 0 —
+// the other 248 threads take it from shared memory instead of each re-reading and re-summing it), the
+// second segment of an odd pair skipped, no per-element bounds branches (columns j >= K are computed
+// on padding and discarded).  Per-accumulator summation order = fin_tile's: bitwise the same result.
+__device__ __forceinline__ double fin_tile_img(const FinParams &p, int b, int j0, int tid, int grp, float (*sU)[kDP + 1],
+                                               float (*sV)[kDP + 1], const int *segs, int nseg, double N,
+                                               double *sS0) {
+  const int jq = tid & 7, kr = tid >> 3;
+  const int nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
+  const size_t seg_stride = (size_t)2 * p.dpad * p.Kp;
+  double S0[4] = {0.0, 0.0, 0.0, 0.0}, S1[kFinKR][4], S2[kFinKR][4];
+#pragma unroll
+  for (int r = 0; r < kFinKR; ++r)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) S1[r][e] = S2[r][e] = 0.0;
+  for (int si = 0; si < nseg; si += 2) {
+    const bool two = si + 1 < nseg;
+    const int ca = segs[si], cb = two ? segs[si + 1] : ca;
+    const float *sa = p.slots + (size_t)seg_slot(ca, b) * seg_stride + jb;
+    const float *sb = p.slots + (size_t)seg_slot(cb, b) * seg_stride + jb;
+    float4 a1[kFinKR], a2[kFinKR], b1[kFinKR], b2[kFinKR], z0[2][4];
+#pragma unroll
+    for (int r = 0; r < kFinKR; ++r) {
+      const size_t k = (size_t)(kr + 32 * r) * p.Kp, k2 = k + (size_t)p.dpad * p.Kp;
+      a1[r] = __ldcs(reinterpret_cast<const float4 *>(sa + k));
+      a2[r] = __ldcs(reinterpret_cast<const float4 *>(sa + k2));
+      if (two) {
+        b1[r] = __ldcs(reinterpret_cast<const float4 *>(sb + k));
+        b2[r] = __ldcs(reinterpret_cast<const float4 *>(sb + k2));
+      }
+    }
+    if (kr == 0) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (u == 0 || two)
+            z0[u][q] = __ldcs(reinterpret_cast<const float4 *>(p.s0slots + ((size_t)seg_slot(u ? cb : ca, b) * 4 + q) * p.Kp + jb));
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (u == 0 || two)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            S0[0] += (double)z0[u][q].x; S0[1] += (double)z0[u][q].y; S0[2] += (double)z0[u][q].z; S0[3] += (double)z0[u][q].w;
+          }
+    }
+#pragma unroll
+    for (int r = 0; r < kFinKR; ++r) {
+      S1[r][0] += (double)a1[r].x; S1[r][1] += (double)a1[r].y; S1[r][2] += (double)a1[r].z; S1[r][3] += (double)a1[r].w;
+      S2[r][0] += (double)a2[r].x; S2[r][1] += (double)a2[r].y; S2[r][2] += (double)a2[r].z; S2[r][3] += (double)a2[r].w;
+    }
+    if (two)
+#pragma unroll
+      for (int r = 0; r < kFinKR; ++r) {
+        S1[r][0] += (double)b1[r].x; S1[r][1] += (double)b1[r].y; S1[r][2] += (double)b1[r].z; S1[r][3] += (double)b1[r].w;
+        S2[r][0] += (double)b2[r].x; S2[r][1] += (double)b2[r].y; S2[r][2] += (double)b2[r].z; S2[r][3] += (double)b2[r].w;
+      }
+  }
+  if (kr == 0)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sS0[jb + e] = S0[e] * (1.0 / (double)kPScale);  // S0 was accumulated from P = gamma 2^14
+  ptx::named_bar_sync(1 + grp, 256);  // this group's S0 of the tile
+#pragma unroll
+  for (int e = 0; e < 4; ++e) S0[e] = sS0[jb + e];
+  double fu[4], fv[4];
+  const double invN = N > 0.0 ? 1.0 / N : 0.0;
+  const bool norm = p.mode == 0 && N > 0.0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    fu[e] = norm ? invN * p.pscale[jb + e] : 1.0;           // 1 / (N sqrt(pi_j))
+    fv[e] = norm ? invN * p.pscale[p.Kp + jb + e] : 1.0;    // 1 / (N sqrt(2 pi_j))
+  }
+  const bool zero = (p.mode != 2) && !(N > 0.0);
+  double ss = 0.0;
+#pragma unroll
+  for (int r = 0; r < kFinKR; ++r) {
+    const int k = kr + 32 * r;
+    if (k >= p.D) continue;
+    const double xs = p.xinv[k];  // 1 / (2^14 2^e_k): powers of two, exact
+    const double *cf = p.coef + (size_t)k * p.Kp + jb;
+    const double2 m01 = *reinterpret_cast<const double2 *>(cf), m23 = *reinterpret_cast<const double2 *>(cf + 2);
+    const double2 i01 = *reinterpret_cast<const double2 *>(cf + kDMax * p.Kp);
+    const double2 i23 = *reinterpret_cast<const double2 *>(cf + kDMax * p.Kp + 2);
+    const double2 v01 = *reinterpret_cast<const double2 *>(cf + 2 * kDMax * p.Kp);
+    const double2 v23 = *reinterpret_cast<const double2 *>(cf + 2 * kDMax * p.Kp + 2);
+    const double mup[4] = {m01.x, m01.y, m23.x, m23.y}, isd[4] = {i01.x, i01.y, i23.x, i23.y},
+                 ivar[4] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double s1 = S1[r][e] * xs, s2 = S2[r][e] * (xs * xs * (double)kPScale);
+      double U = (s1 - mup[e] * S0[e]) * isd[e];                                      // sum gamma (x - mu)/sd
+      double V = (s2 - 2.0 * mup[e] * s1 + mup[e] * mup[e] * S0[e]) * ivar[e] - S0[e];  // ((x-mu)^2/var - 1)
+      float u, v;
+      if (p.mode != 2) {
+        U = zero ? 0.0 : U * fu[e];
+        V = zero ? 0.0 : V * fv[e];
+        if (4 * jq + e < nj) ss += fabs(U) + fabs(V);  // = (signed sqrt)^2
+        u = signed_sqrt((float)U);
+        v = signed_sqrt((float)V);
+      } else {
+        u = (float)U;
+        v = (float)V;
+      }
+      sU[4 * jq + e][k] = u;  // rows j >= K (padding) are never read
+      sV[4 * jq + e][k] = v;
+    }
+  }
+  return ss;
+}
+
 // Whole-image finalize for large batches (D <= 64, K <= 256): persistent blocks of 512 threads take
 // whole images; the two 256-thread groups compute the image's (32 x 64) tiles with fin_tile into a
 // shared-memory copy of the image (2 x 256 x 65 floats), the block reduces the squared norm in a fixed
@@ -617,6 +728,7 @@ __global__ void __launch_bounds__(256, 3) k_finalize(const FinParams p) {
 constexpr int kImgK = 256;
 constexpr int kImgThreads = 512;
 constexpr int kImgSmemBytes = 2 * kImgK * (kDP + 1) * 4;
+constexpr int kImgMaxSeg = 160;  // segment list capacity per image (>= clusters of any launch)
 template <bool kScore>
 __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams p) {
   ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
@@ -628,9 +740,27 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
   const int tid = threadIdx.x, grp = tid >> 8, gt = tid & 255, lane = tid & 31, warp = tid >> 5;
   const int KD = p.K * p.D, ntiles = (p.K + kFinJ - 1) / kFinJ;
   const bool l2 = p.mode != 2;
+  __shared__ int s_segs[kImgMaxSeg];
+  __shared__ int s_nseg;
+  __shared__ double s_S0[kImgK];
   for (int b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    if (p.slots && tid == 0) {  // the image's non-empty (cluster) segments, once for all its tiles
+      const int ft = (int)p.tile_start[b], lt = (int)p.tile_start[b + 1];
+      const int clo = p.cown[2 * b], chi = p.cown[2 * b + 1];
+      int ns = 0;
+      for (int c = clo; c <= chi && ns < kImgMaxSeg; ++c) {
+        const int st = p.cstart[c], en = p.cstart[c + 1];
+        if ((st > ft ? st : ft) < (en < lt ? en : lt)) s_segs[ns++] = c;
+      }
+      s_nseg = ns;
+    }
+    __syncthreads();
+    const bool use_list = p.slots && s_nseg < kImgMaxSeg;  // (a longer list falls back to the scan)
+    const double N = p.slots ? (double)(p.offsets[b + 1] - p.offsets[b]) : 0.0;
     double ss = 0.0;
-    for (int t = grp; t < ntiles; t += kImgThreads / 256) ss += fin_tile(p, b, t * kFinJ, 0, gt, iU + t * kFinJ, iV + t * kFinJ);
+    for (int t = grp; t < ntiles; t += kImgThreads / 256)
+      ss += use_list ? fin_tile_img(p, b, t * kFinJ, gt, grp, iU + t * kFinJ, iV + t * kFinJ, s_segs, s_nseg, N, s_S0)
+                     : fin_tile(p, b, t * kFinJ, 0, gt, iU + t * kFinJ, iV + t * kFinJ);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
     if (lane == 0) s_red[warp] = ss;
@@ -638,15 +768,17 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
     double n2 = 0.0;  // fixed order: bitwise repeatable
     for (int w = 0; w < kImgThreads / 32; ++w) n2 += s_red[w];
     const float sc = (l2 && n2 > 0.0) ? (float)(1.0 / sqrt(n2)) : 1.f;
+    // the image's (j, k) elements: row j by one warp, lanes over k (coalesced, no index division)
     if (kScore) {
       for (int c = 0; c < p.n_cls; ++c) {
         const float *wc = p.svm_w + (size_t)c * 2 * KD;
         float a = 0.f;
-        for (int e = tid; e < KD; e += kImgThreads) {
-          const int j = e / p.D, k = e - j * p.D;
-          a = fmaf(iU[j][k], __ldg(wc + e), a);
-          a = fmaf(iV[j][k], __ldg(wc + KD + e), a);
-        }
+        for (int j = warp; j < p.K; j += kImgThreads / 32)
+          for (int k = lane; k < p.D; k += 32) {
+            const int e = j * p.D + k;
+            a = fmaf(iU[j][k], __ldg(wc + e), a);
+            a = fmaf(iV[j][k], __ldg(wc + KD + e), a);
+          }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
         if (lane == 0) s_dot[warp][c] = a;
@@ -661,13 +793,27 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
     }
     if (!kScore || p.out) {
       float *o = p.out + (size_t)b * 2 * KD;
-      for (int e = tid; e < KD; e += kImgThreads) {
-        const int j = e / p.D, k = e - j * p.D;
-        o[e] = iU[j][k] * sc;
-        o[KD + e] = iV[j][k] * sc;
+      if (p.D == kDP) {  // two rows per warp per step, no bounds checks on k
+        for (int j = warp; j < p.K; j += 2 * (kImgThreads / 32)) {
+          const int j2 = j + kImgThreads / 32;
+          const float u0 = iU[j][lane] * sc, u1 = iU[j][lane + 32] * sc, v0 = iV[j][lane] * sc, v1 = iV[j][lane + 32] * sc;
+          o[j * kDP + lane] = u0; o[j * kDP + lane + 32] = u1;
+          o[KD + j * kDP + lane] = v0; o[KD + j * kDP + lane + 32] = v1;
+          if (j2 < p.K) {
+            const float a0 = iU[j2][lane] * sc, a1 = iU[j2][lane + 32] * sc, c0 = iV[j2][lane] * sc, c1 = iV[j2][lane + 32] * sc;
+            o[j2 * kDP + lane] = a0; o[j2 * kDP + lane + 32] = a1;
+            o[KD + j2 * kDP + lane] = c0; o[KD + j2 * kDP + lane + 32] = c1;
+          }
+        }
+      } else {
+        for (int j = warp; j < p.K; j += kImgThreads / 32)
+          for (int k = lane; k < p.D; k += 32) {
+            o[j * p.D + k] = iU[j][k] * sc;
+            o[KD + j * p.D + k] = iV[j][k] * sc;
+          }
       }
     }
-    __syncthreads();  // the next image overwrites the shared image and s_red
+    __syncthreads();  // the next image overwrites the shared image, s_red, s_S0 and the segment list
   }
 }
 
