@@ -615,8 +615,8 @@ __global__ void __launch_bounds__(256, 2) k_finalize(const FinParams p) {
 // second segment of an odd pair skipped, no per-element bounds branches (columns j >= K are computed
 // on padding and discarded).  Per-accumulator summation order = fin_tile's: bitwise the same result.
 __device__ __forceinline__ double fin_tile_img(const FinParams &p, int b, int j0, int tid, int grp, float (*sU)[kDP + 1],
-                                               float (*sV)[kDP + 1], const int *segs, int nseg, double N,
-                                               double *sS0) {
+                                               float (*sV)[kDP + 1], const int *segs, int cfirst, int nseg,
+                                               double N, double *sS0) {
   const int jq = tid & 7, kr = tid >> 3;
   const int nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
   const size_t seg_stride = (size_t)2 * p.dpad * p.Kp;
@@ -627,7 +627,7 @@ __device__ __forceinline__ double fin_tile_img(const FinParams &p, int b, int j0
     for (int e = 0; e < 4; ++e) S1[r][e] = S2[r][e] = 0.0;
   for (int si = 0; si < nseg; si += 2) {
     const bool two = si + 1 < nseg;
-    const int ca = segs[si], cb = two ? segs[si + 1] : ca;
+    const int ca = segs ? segs[si] : cfirst + si, cb = two ? (segs ? segs[si + 1] : ca + 1) : ca;
     const float *sa = p.slots + (size_t)seg_slot(ca, b) * seg_stride + jb;
     const float *sb = p.slots + (size_t)seg_slot(cb, b) * seg_stride + jb;
     float4 a1[kFinKR], a2[kFinKR], b1[kFinKR], b2[kFinKR], z0[2][4];
@@ -743,8 +743,35 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
   __shared__ int s_segs[kImgMaxSeg];
   __shared__ int s_nseg;
   __shared__ double s_S0[kImgK];
-  for (int b = blockIdx.x; b < p.batch; b += gridDim.x) {
-    if (p.slots && tid == 0) {  // the image's non-empty (cluster) segments, once for all its tiles
+  // With every cluster non-empty (T >= ncl) the segments of image b are exactly clusters
+  // cown[2b] .. cown[2b+1]: no scan.  That range and N of the images ahead of the current one are
+  // kept in a ring (thread 0 reads image b + 2 gridDim.x while b is processed) so that at the top of
+  // image b thread 0 can bulk-prefetch the next image's slots into L2 without waiting on any load.
+  __shared__ __align__(8) int s_lh[3][2];
+  __shared__ int64_t s_off[3][2];
+  const bool direct = p.slots && p.tile_start[p.batch] >= (int64_t)p.ncl;
+  const size_t seg_bytes = (size_t)2 * p.dpad * p.Kp * 4, s0_bytes = (size_t)4 * p.Kp * 4;
+  auto info = [&](int bb, int slot) {  // thread 0 only: cown range and offsets of image bb, asynchronously
+    if (bb < p.batch) {
+      ptx::cp_async8(&s_lh[slot][0], p.cown + 2 * bb);
+      ptx::cp_async8(&s_off[slot][0], p.offsets + bb);
+      ptx::cp_async8(&s_off[slot][1], p.offsets + bb + 1);
+    }
+  };
+  if (direct && tid == 0) { info(blockIdx.x, 0); info(blockIdx.x + gridDim.x, 1); ptx::cp_async_wait_all(); }
+  __syncthreads();
+  for (int b = blockIdx.x, it = 0; b < p.batch; b += gridDim.x, ++it) {
+    const int cur = it % 3, nxt = (it + 1) % 3, far = (it + 2) % 3;
+    if (direct && tid == 0) {
+      if (b + (int)gridDim.x < p.batch)
+        for (int c = s_lh[nxt][0]; c <= s_lh[nxt][1]; ++c) {  // the next image's segments -> L2
+          const int64_t sl = seg_slot(c, b + gridDim.x);
+          ptx::prefetch_l2_bulk(p.slots + sl * (seg_bytes / 4), (uint32_t)seg_bytes);
+          ptx::prefetch_l2_bulk(p.s0slots + sl * (s0_bytes / 4), (uint32_t)s0_bytes);
+        }
+      info(b + 2 * gridDim.x, far);  // arrives while this image is processed
+    }
+    if (!direct && p.slots && tid == 0) {  // the image's non-empty (cluster) segments, once for all its tiles
       const int ft = (int)p.tile_start[b], lt = (int)p.tile_start[b + 1];
       const int clo = p.cown[2 * b], chi = p.cown[2 * b + 1];
       int ns = 0;
@@ -754,12 +781,15 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
       }
       s_nseg = ns;
     }
-    __syncthreads();
-    const bool use_list = p.slots && s_nseg < kImgMaxSeg;  // (a longer list falls back to the scan)
-    const double N = p.slots ? (double)(p.offsets[b + 1] - p.offsets[b]) : 0.0;
+    if (!direct) __syncthreads();
+    const bool use_list = p.slots && (direct || s_nseg < kImgMaxSeg);  // (a longer list falls back to the scan)
+    const int cfirst = direct ? s_lh[cur][0] : 0, nseg = direct ? s_lh[cur][1] - s_lh[cur][0] + 1 : (p.slots ? s_nseg : 0);
+    const double N = direct ? (double)(s_off[cur][1] - s_off[cur][0])
+                            : (p.slots ? (double)(p.offsets[b + 1] - p.offsets[b]) : 0.0);
     double ss = 0.0;
     for (int t = grp; t < ntiles; t += kImgThreads / 256)
-      ss += use_list ? fin_tile_img(p, b, t * kFinJ, gt, grp, iU + t * kFinJ, iV + t * kFinJ, s_segs, s_nseg, N, s_S0)
+      ss += use_list ? fin_tile_img(p, b, t * kFinJ, gt, grp, iU + t * kFinJ, iV + t * kFinJ, direct ? nullptr : s_segs,
+                                    cfirst, nseg, N, s_S0)
                      : fin_tile(p, b, t * kFinJ, 0, gt, iU + t * kFinJ, iV + t * kFinJ);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
@@ -813,6 +843,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
           }
       }
     }
+    if (direct && tid == 0) ptx::cp_async_wait_all();
     __syncthreads();  // the next image overwrites the shared image, s_red, s_S0 and the segment list
   }
 }

@@ -198,6 +198,21 @@ __device__ __forceinline__ void st_async_v2f32(uint32_t remote_addr, float a, fl
                "f"(a), "f"(b), "r"(remote_bar)
                : "memory");
 }
+// Asynchronous global -> shared copies of 4 / 8 bytes (LDGSTS: no registers held while in flight),
+// completed by cp_async_wait_all() of the issuing thread.
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Bulk prefetch of [ptr, ptr + bytes) into L2 (no shared memory, no registers); bytes % 16 == 0.
+__device__ __forceinline__ void prefetch_l2_bulk(const void *ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
