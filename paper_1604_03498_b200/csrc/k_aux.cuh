@@ -450,6 +450,119 @@ __device__ __forceinline__ double fin_tile(const FinParams &p, int b, int j0, in
   return ss;
 }
 
+// fin_tile over a known segment range / list (slots mode): one round of loads per segment pair (S1
+// and S2 of every thread, S0 of the 4 Gaussians by the 8 threads with kr == 0 — the other 248 threads
+// take it from shared memory sS0[j - s0base] instead of each re-reading and re-summing it), the second
+// segment of an odd pair skipped, no per-element bounds branches (columns j >= K are computed on
+// padding and discarded).  Segment i is segs[i], or cfirst + i when segs == nullptr.  The 256 threads
+// of the tile meet once on named barrier bar_id.  Per-accumulator summation order = fin_tile's:
+// bitwise the same result.
+__device__ __forceinline__ double fin_tile_seg(const FinParams &p, int b, int j0, int kb, int tid, int bar_id,
+                                               float (*sU)[kDP + 1], float (*sV)[kDP + 1], const int *segs,
+                                               int cfirst, int nseg, double N, double *sS0, int s0base) {
+  const int jq = tid & 7, kr = (tid >> 3) + kb;
+  const int nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
+  const size_t seg_stride = (size_t)2 * p.dpad * p.Kp;
+  double S0[4] = {0.0, 0.0, 0.0, 0.0}, S1[kFinKR][4], S2[kFinKR][4];
+#pragma unroll
+  for (int r = 0; r < kFinKR; ++r)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) S1[r][e] = S2[r][e] = 0.0;
+  for (int si = 0; si < nseg; si += 2) {
+    const bool two = si + 1 < nseg;
+    const int ca = segs ? segs[si] : cfirst + si, cb = two ? (segs ? segs[si + 1] : ca + 1) : ca;
+    const float *sa = p.slots + (size_t)seg_slot(ca, b) * seg_stride + jb;
+    const float *sb = p.slots + (size_t)seg_slot(cb, b) * seg_stride + jb;
+    float4 a1[kFinKR], a2[kFinKR], b1[kFinKR], b2[kFinKR], z0[2][4];
+#pragma unroll
+    for (int r = 0; r < kFinKR; ++r) {
+      const size_t k = (size_t)(kr + 32 * r) * p.Kp, k2 = k + (size_t)p.dpad * p.Kp;
+      a1[r] = __ldcs(reinterpret_cast<const float4 *>(sa + k));
+      a2[r] = __ldcs(reinterpret_cast<const float4 *>(sa + k2));
+      if (two) {
+        b1[r] = __ldcs(reinterpret_cast<const float4 *>(sb + k));
+        b2[r] = __ldcs(reinterpret_cast<const float4 *>(sb + k2));
+      }
+    }
+    if (kr == kb) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (u == 0 || two)
+            z0[u][q] = __ldcs(reinterpret_cast<const float4 *>(p.s0slots + ((size_t)seg_slot(u ? cb : ca, b) * 4 + q) * p.Kp + jb));
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (u == 0 || two)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            S0[0] += (double)z0[u][q].x; S0[1] += (double)z0[u][q].y; S0[2] += (double)z0[u][q].z; S0[3] += (double)z0[u][q].w;
+          }
+    }
+#pragma unroll
+    for (int r = 0; r < kFinKR; ++r) {
+      S1[r][0] += (double)a1[r].x; S1[r][1] += (double)a1[r].y; S1[r][2] += (double)a1[r].z; S1[r][3] += (double)a1[r].w;
+      S2[r][0] += (double)a2[r].x; S2[r][1] += (double)a2[r].y; S2[r][2] += (double)a2[r].z; S2[r][3] += (double)a2[r].w;
+    }
+    if (two)
+#pragma unroll
+      for (int r = 0; r < kFinKR; ++r) {
+        S1[r][0] += (double)b1[r].x; S1[r][1] += (double)b1[r].y; S1[r][2] += (double)b1[r].z; S1[r][3] += (double)b1[r].w;
+        S2[r][0] += (double)b2[r].x; S2[r][1] += (double)b2[r].y; S2[r][2] += (double)b2[r].z; S2[r][3] += (double)b2[r].w;
+      }
+  }
+  if (kr == kb)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sS0[jb + e - s0base] = S0[e] * (1.0 / (double)kPScale);  // S0 was accumulated from P = gamma 2^14
+  ptx::named_bar_sync(bar_id, 256);  // the tile's S0
+#pragma unroll
+  for (int e = 0; e < 4; ++e) S0[e] = sS0[jb + e - s0base];
+  double fu[4], fv[4];
+  const double invN = N > 0.0 ? 1.0 / N : 0.0;
+  const bool norm = p.mode == 0 && N > 0.0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    fu[e] = norm ? invN * p.pscale[jb + e] : 1.0;           // 1 / (N sqrt(pi_j))
+    fv[e] = norm ? invN * p.pscale[p.Kp + jb + e] : 1.0;    // 1 / (N sqrt(2 pi_j))
+  }
+  const bool zero = (p.mode != 2) && !(N > 0.0);
+  double ss = 0.0;
+#pragma unroll
+  for (int r = 0; r < kFinKR; ++r) {
+    const int k = kr + 32 * r;
+    if (k >= p.D) continue;
+    const double xs = p.xinv[k];  // 1 / (2^14 2^e_k): powers of two, exact
+    const double *cf = p.coef + (size_t)k * p.Kp + jb;
+    const double2 m01 = *reinterpret_cast<const double2 *>(cf), m23 = *reinterpret_cast<const double2 *>(cf + 2);
+    const double2 i01 = *reinterpret_cast<const double2 *>(cf + kDMax * p.Kp);
+    const double2 i23 = *reinterpret_cast<const double2 *>(cf + kDMax * p.Kp + 2);
+    const double2 v01 = *reinterpret_cast<const double2 *>(cf + 2 * kDMax * p.Kp);
+    const double2 v23 = *reinterpret_cast<const double2 *>(cf + 2 * kDMax * p.Kp + 2);
+    const double mup[4] = {m01.x, m01.y, m23.x, m23.y}, isd[4] = {i01.x, i01.y, i23.x, i23.y},
+                 ivar[4] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double s1 = S1[r][e] * xs, s2 = S2[r][e] * (xs * xs * (double)kPScale);
+      double U = (s1 - mup[e] * S0[e]) * isd[e];                                      // sum gamma (x - mu)/sd
+      double V = (s2 - 2.0 * mup[e] * s1 + mup[e] * mup[e] * S0[e]) * ivar[e] - S0[e];  // ((x-mu)^2/var - 1)
+      float u, v;
+      if (p.mode != 2) {
+        U = zero ? 0.0 : U * fu[e];
+        V = zero ? 0.0 : V * fv[e];
+        if (4 * jq + e < nj) ss += fabs(U) + fabs(V);  // = (signed sqrt)^2
+        u = signed_sqrt((float)U);
+        v = signed_sqrt((float)V);
+      } else {
+        u = (float)U;
+        v = (float)V;
+      }
+      sU[4 * jq + e][k - kb] = u;  // rows j >= K (padding) are never read
+      sV[4 * jq + e][k - kb] = v;
+    }
+  }
+  return ss;
+}
+
 // grid (ceil(K/32), batch), 256 threads.  Thread (jq = tid % 8, kr = tid / 8) owns Gaussians
 // j0 + 4 jq .. +3 and dims kr, kr + 32: every slot / coefficient read is a 16-byte vector, coalesced
 // over jq (the slots are feature-major rows of Kp Gaussians); U/V go through a shared-memory tile so
@@ -475,7 +588,15 @@ __global__ void __launch_bounds__(256, 2) k_finalize(const FinParams p) {
   const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0);
   const int kb = kDP * (int)blockIdx.z, nk = min(kDP, p.D - kb);  // this block's dims [kb, kb + nk)
   const int KD = p.K * p.D;
-  double ss = fin_tile(p, b, j0, kb, tid, sU, sV);
+  double ss;
+  if (p.slots && p.tile_start[p.batch] >= (int64_t)p.ncl) {  // every cluster non-empty: segments = cown range
+    __shared__ double s_S0[kFinJ];
+    const int lo = p.cown[2 * b], hi = p.cown[2 * b + 1];
+    ss = fin_tile_seg(p, b, j0, kb, tid, 1, sU, sV, nullptr, lo, hi - lo + 1,
+                      (double)(p.offsets[b + 1] - p.offsets[b]), s_S0, j0);
+  } else {
+    ss = fin_tile(p, b, j0, kb, tid, sU, sV);
+  }
   __syncthreads();
   const int part = blockIdx.z * gridDim.x + blockIdx.x, nparts = gridDim.x * gridDim.z;
   if (!kSync && (!kScore || p.out)) {
@@ -609,117 +730,6 @@ __global__ void __launch_bounds__(256, 2) k_finalize(const FinParams p) {
   }
 }
 
-// fin_tile for k_finalize_img (slots mode, segment list of the image precomputed): one round of loads
-// per segment pair (S1 and S2 of every thread, S0 of the 4 Gaussians by the 8 threads with kr == 0 —
-// the other 248 threads take it from shared memory instead of each re-reading and re-summing it), the
-// second segment of an odd pair skipped, no per-element bounds branches (columns j >= K are computed
-// on padding and discarded).  Per-accumulator summation order = fin_tile's: bitwise the same result.
-__device__ __forceinline__ double fin_tile_img(const FinParams &p, int b, int j0, int tid, int grp, float (*sU)[kDP + 1],
-                                               float (*sV)[kDP + 1], const int *segs, int cfirst, int nseg,
-                                               double N, double *sS0) {
-  const int jq = tid & 7, kr = tid >> 3;
-  const int nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
-  const size_t seg_stride = (size_t)2 * p.dpad * p.Kp;
-  double S0[4] = {0.0, 0.0, 0.0, 0.0}, S1[kFinKR][4], S2[kFinKR][4];
-#pragma unroll
-  for (int r = 0; r < kFinKR; ++r)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) S1[r][e] = S2[r][e] = 0.0;
-  for (int si = 0; si < nseg; si += 2) {
-    const bool two = si + 1 < nseg;
-    const int ca = segs ? segs[si] : cfirst + si, cb = two ? (segs ? segs[si + 1] : ca + 1) : ca;
-    const float *sa = p.slots + (size_t)seg_slot(ca, b) * seg_stride + jb;
-    const float *sb = p.slots + (size_t)seg_slot(cb, b) * seg_stride + jb;
-    float4 a1[kFinKR], a2[kFinKR], b1[kFinKR], b2[kFinKR], z0[2][4];
-#pragma unroll
-    for (int r = 0; r < kFinKR; ++r) {
-      const size_t k = (size_t)(kr + 32 * r) * p.Kp, k2 = k + (size_t)p.dpad * p.Kp;
-      a1[r] = __ldcs(reinterpret_cast<const float4 *>(sa + k));
-      a2[r] = __ldcs(reinterpret_cast<const float4 *>(sa + k2));
-      if (two) {
-        b1[r] = __ldcs(reinterpret_cast<const float4 *>(sb + k));
-        b2[r] = __ldcs(reinterpret_cast<const float4 *>(sb + k2));
-      }
-    }
-    if (kr == 0) {
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (u == 0 || two)
-            z0[u][q] = __ldcs(reinterpret_cast<const float4 *>(p.s0slots + ((size_t)seg_slot(u ? cb : ca, b) * 4 + q) * p.Kp + jb));
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-        if (u == 0 || two)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            S0[0] += (double)z0[u][q].x; S0[1] += (double)z0[u][q].y; S0[2] += (double)z0[u][q].z; S0[3] += (double)z0[u][q].w;
-          }
-    }
-#pragma unroll
-    for (int r = 0; r < kFinKR; ++r) {
-      S1[r][0] += (double)a1[r].x; S1[r][1] += (double)a1[r].y; S1[r][2] += (double)a1[r].z; S1[r][3] += (double)a1[r].w;
-      S2[r][0] += (double)a2[r].x; S2[r][1] += (double)a2[r].y; S2[r][2] += (double)a2[r].z; S2[r][3] += (double)a2[r].w;
-    }
-    if (two)
-#pragma unroll
-      for (int r = 0; r < kFinKR; ++r) {
-        S1[r][0] += (double)b1[r].x; S1[r][1] += (double)b1[r].y; S1[r][2] += (double)b1[r].z; S1[r][3] += (double)b1[r].w;
-        S2[r][0] += (double)b2[r].x; S2[r][1] += (double)b2[r].y; S2[r][2] += (double)b2[r].z; S2[r][3] += (double)b2[r].w;
-      }
-  }
-  if (kr == 0)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) sS0[jb + e] = S0[e] * (1.0 / (double)kPScale);  // S0 was accumulated from P = gamma 2^14
-  ptx::named_bar_sync(1 + grp, 256);  // this group's S0 of the tile
-#pragma unroll
-  for (int e = 0; e < 4; ++e) S0[e] = sS0[jb + e];
-  double fu[4], fv[4];
-  const double invN = N > 0.0 ? 1.0 / N : 0.0;
-  const bool norm = p.mode == 0 && N > 0.0;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    fu[e] = norm ? invN * p.pscale[jb + e] : 1.0;           // 1 / (N sqrt(pi_j))
-    fv[e] = norm ? invN * p.pscale[p.Kp + jb + e] : 1.0;    // 1 / (N sqrt(2 pi_j))
-  }
-  const bool zero = (p.mode != 2) && !(N > 0.0);
-  double ss = 0.0;
-#pragma unroll
-  for (int r = 0; r < kFinKR; ++r) {
-    const int k = kr + 32 * r;
-    if (k >= p.D) continue;
-    const double xs = p.xinv[k];  // 1 / (2^14 2^e_k): powers of two, exact
-    const double *cf = p.coef + (size_t)k * p.Kp + jb;
-    const double2 m01 = *reinterpret_cast<const double2 *>(cf), m23 = *reinterpret_cast<const double2 *>(cf + 2);
-    const double2 i01 = *reinterpret_cast<const double2 *>(cf + kDMax * p.Kp);
-    const double2 i23 = *reinterpret_cast<const double2 *>(cf + kDMax * p.Kp + 2);
-    const double2 v01 = *reinterpret_cast<const double2 *>(cf + 2 * kDMax * p.Kp);
-    const double2 v23 = *reinterpret_cast<const double2 *>(cf + 2 * kDMax * p.Kp + 2);
-    const double mup[4] = {m01.x, m01.y, m23.x, m23.y}, isd[4] = {i01.x, i01.y, i23.x, i23.y},
-                 ivar[4] = {v01.x, v01.y, v23.x, v23.y};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const double s1 = S1[r][e] * xs, s2 = S2[r][e] * (xs * xs * (double)kPScale);
-      double U = (s1 - mup[e] * S0[e]) * isd[e];                                      // sum gamma (x - mu)/sd
-      double V = (s2 - 2.0 * mup[e] * s1 + mup[e] * mup[e] * S0[e]) * ivar[e] - S0[e];  // ((x-mu)^2/var - 1)
-      float u, v;
-      if (p.mode != 2) {
-        U = zero ? 0.0 : U * fu[e];
-        V = zero ? 0.0 : V * fv[e];
-        if (4 * jq + e < nj) ss += fabs(U) + fabs(V);  // = (signed sqrt)^2
-        u = signed_sqrt((float)U);
-        v = signed_sqrt((float)V);
-      } else {
-        u = (float)U;
-        v = (float)V;
-      }
-      sU[4 * jq + e][k] = u;  // rows j >= K (padding) are never read
-      sV[4 * jq + e][k] = v;
-    }
-  }
-  return ss;
-}
-
 // Whole-image finalize for large batches (D <= 64, K <= 256): persistent blocks of 512 threads take
 // whole images; the two 256-thread groups compute the image's (32 x 64) tiles with fin_tile into a
 // shared-memory copy of the image (2 x 256 x 65 floats), the block reduces the squared norm in a fixed
@@ -788,8 +798,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
                             : (p.slots ? (double)(p.offsets[b + 1] - p.offsets[b]) : 0.0);
     double ss = 0.0;
     for (int t = grp; t < ntiles; t += kImgThreads / 256)
-      ss += use_list ? fin_tile_img(p, b, t * kFinJ, gt, grp, iU + t * kFinJ, iV + t * kFinJ, direct ? nullptr : s_segs,
-                                    cfirst, nseg, N, s_S0)
+      ss += use_list ? fin_tile_seg(p, b, t * kFinJ, 0, gt, 1 + grp, iU + t * kFinJ, iV + t * kFinJ,
+                                    direct ? nullptr : s_segs, cfirst, nseg, N, s_S0, 0)
                      : fin_tile(p, b, t * kFinJ, 0, gt, iU + t * kFinJ, iV + t * kFinJ);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
