@@ -451,8 +451,8 @@ __device__ __forceinline__ double fin_tile(const FinParams &p, int b, int j0, in
 }
 
 // fin_tile over a known segment range / list (slots mode): one round of loads per segment pair (S1
-// and S2 of every thread, S0 of the 4 Gaussians by the 8 threads with kr == 0 — the other 248 threads
-// take it from shared memory sS0[j - s0base] instead of each re-reading and re-summing it), the second
+// and S2 of every thread; S0 of the tile's 32 Gaussians by the first warp, one Gaussian per lane — the
+// other threads take it from shared memory sS0[j - s0base] instead of each re-summing it), the second
 // segment of an odd pair skipped, no per-element bounds branches (columns j >= K are computed on
 // padding and discarded).  Segment i is segs[i], or cfirst + i when segs == nullptr.  The 256 threads
 // of the tile meet once on named barrier bar_id.  Per-accumulator summation order = fin_tile's:
@@ -463,7 +463,7 @@ __device__ __forceinline__ double fin_tile_seg(const FinParams &p, int b, int j0
   const int jq = tid & 7, kr = (tid >> 3) + kb;
   const int nj = min(kFinJ, p.K - j0), jb = j0 + 4 * jq;
   const size_t seg_stride = (size_t)2 * p.dpad * p.Kp;
-  double S0[4] = {0.0, 0.0, 0.0, 0.0}, S1[kFinKR][4], S2[kFinKR][4];
+  double S0l = 0.0, S0[4], S1[kFinKR][4], S2[kFinKR][4];
 #pragma unroll
   for (int r = 0; r < kFinKR; ++r)
 #pragma unroll
@@ -473,7 +473,8 @@ __device__ __forceinline__ double fin_tile_seg(const FinParams &p, int b, int j0
     const int ca = segs ? segs[si] : cfirst + si, cb = two ? (segs ? segs[si + 1] : ca + 1) : ca;
     const float *sa = p.slots + (size_t)seg_slot(ca, b) * seg_stride + jb;
     const float *sb = p.slots + (size_t)seg_slot(cb, b) * seg_stride + jb;
-    float4 a1[kFinKR], a2[kFinKR], b1[kFinKR], b2[kFinKR], z0[2][4];
+    float4 a1[kFinKR], a2[kFinKR], b1[kFinKR], b2[kFinKR];
+    float z0[2][4];
 #pragma unroll
     for (int r = 0; r < kFinKR; ++r) {
       const size_t k = (size_t)(kr + 32 * r) * p.Kp, k2 = k + (size_t)p.dpad * p.Kp;
@@ -484,20 +485,17 @@ __device__ __forceinline__ double fin_tile_seg(const FinParams &p, int b, int j0
         b2[r] = __ldcs(reinterpret_cast<const float4 *>(sb + k2));
       }
     }
-    if (kr == kb) {
+    if (tid < 32) {  // S0 of Gaussian j0 + tid: 4 row-group partials per segment
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (u == 0 || two)
-            z0[u][q] = __ldcs(reinterpret_cast<const float4 *>(p.s0slots + ((size_t)seg_slot(u ? cb : ca, b) * 4 + q) * p.Kp + jb));
+          if (u == 0 || two) z0[u][q] = __ldcs(p.s0slots + ((size_t)seg_slot(u ? cb : ca, b) * 4 + q) * p.Kp + j0 + tid);
 #pragma unroll
       for (int u = 0; u < 2; ++u)
         if (u == 0 || two)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            S0[0] += (double)z0[u][q].x; S0[1] += (double)z0[u][q].y; S0[2] += (double)z0[u][q].z; S0[3] += (double)z0[u][q].w;
-          }
+          for (int q = 0; q < 4; ++q) S0l += (double)z0[u][q];
     }
 #pragma unroll
     for (int r = 0; r < kFinKR; ++r) {
@@ -511,9 +509,7 @@ __device__ __forceinline__ double fin_tile_seg(const FinParams &p, int b, int j0
         S2[r][0] += (double)b2[r].x; S2[r][1] += (double)b2[r].y; S2[r][2] += (double)b2[r].z; S2[r][3] += (double)b2[r].w;
       }
   }
-  if (kr == kb)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) sS0[jb + e - s0base] = S0[e] * (1.0 / (double)kPScale);  // S0 was accumulated from P = gamma 2^14
+  if (tid < 32) sS0[j0 + tid - s0base] = S0l * (1.0 / (double)kPScale);  // S0 was accumulated from P = gamma 2^14
   ptx::named_bar_sync(bar_id, 256);  // the tile's S0
 #pragma unroll
   for (int e = 0; e < 4; ++e) S0[e] = sS0[jb + e - s0base];

@@ -26,3 +26,8 @@ timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k re
   -o gpurun_out/${TAG}_embed python bench.py --workload embed --frames 256 --steps 1 --warmup 3 \
   > gpurun_out/${TAG}_embed.log 2>&1
 tail -1 gpurun_out/${TAG}_embed.log
+# single-frame latency path (C2 shape): per-kernel durations of the prepared encode (serialised)
+PROBE_REPS=3 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 12 --csv \
+  --log-file gpurun_out/${TAG}_latency_launches.csv python tools/latency_probe.py > gpurun_out/${TAG}_latency.log 2>&1
+python tools/latency_probe.py >> gpurun_out/${TAG}_latency.log 2>&1
+tail -1 gpurun_out/${TAG}_latency.log
