@@ -131,6 +131,27 @@ def test_batched_ragged_with_empty_images(fv):
                 assert rel_l2(out[b], ref[b]) <= FV_RTOL, (b, n, rel_l2(out[b], ref[b]))
 
 
+@pytest.mark.parametrize("batch", [40, 600])
+def test_mostly_empty_batch_segment_scan(fv, batch):
+    """Far fewer tiles than clusters (T < ncl: most images empty), so some clusters own no tile and
+    the finalize takes the segment-scan path instead of the owner-table range; 600
+    images use the whole-image finalize, 40 the tile-parallel one.  Both are checked against the
+    oracle, and the empty images must come out exactly zero."""
+    gmm_np = fvgen.make_gmm(256, 64, seed=1604)
+    rng = np.random.default_rng(77 + batch)
+    counts = [0] * batch
+    for b in rng.choice(batch, 6, replace=False):
+        counts[b] = int(rng.integers(1, 300))
+    X, off = fvgen.make_batch(gmm_np, counts, seed_base=700 + batch)
+    out = fv.encode_batched(dev(X), dev(off), fv.GMM(*gmm_np), threshold=TAU).cpu().numpy()
+    ref = oracle.encode_batched(X, off, *gmm_np, threshold=TAU)
+    for b, n in enumerate(counts):
+        if n == 0:
+            assert np.all(out[b] == 0)
+        else:
+            assert rel_l2(out[b], ref[b]) <= FV_RTOL, (b, n, rel_l2(out[b], ref[b]))
+
+
 def test_batched_equals_per_image_and_deterministic(fv):
     gmm_np = fvgen.make_gmm(256, 64, seed=1604)
     X, off = fvgen.make_batch(gmm_np, [3000, 257, 4096], seed_base=5)
