@@ -206,9 +206,12 @@ __device__ __forceinline__ void work_wait(uint64_t *bar, uint32_t parity) {
 #define TR(slot) do { if (p.trace && cid == 0 && rank == 0 && i < 64) p.trace[i * 16 + (slot)] = clock64(); } while (0)
 #define TRW(slot) do { if (p.trace && cid == 0 && rank == 0 && i < 64 && lane == 0 && (warp == 0 || warp == 5 || warp == 10 || warp == 15)) \
     p.trace[1024 + ((i * 4 + (warp == 0 ? 0 : warp == 5 ? 1 : warp == 10 ? 2 : 3)) * 16) + (slot)] = clock64(); } while (0)
+// kernel-level points (prologue / epilogue) of CTA 0: slots 7680 + 0..15, written by one thread each
+#define TRP(slot) do { if (p.trace && cid == 0 && rank == 0) p.trace[7680 + (slot)] = clock64(); } while (0)
 #else
 #define TR(slot) do { } while (0)
 #define TRW(slot) do { } while (0)
+#define TRP(slot) do { } while (0)
 #endif
 
 template <bool kD64>
@@ -231,6 +234,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   const uint32_t rank = cluster_ctarank(), C = cluster_nctarank();
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
 
+  if (tid == 0) TRP(0);
   // ---------------- setup
   {
     for (int i = tid; i < kG; i += kThreads2) s_bias[i] = p.bias[rank * kG + i];
@@ -258,9 +262,12 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+  if (tid == 0) TRP(1);
   cluster_sync();
+  if (tid == 0) TRP(2);
   griddep_launch_dependents();  // k_finalize may start its prologue
   griddep_wait();               // k_schedule's tile prefix sums are complete and visible
+  if (tid == 0) TRP(3);
 
   const int64_t T = p.tile_start[p.batch];
   const int t0 = (int)((int64_t)cid * T / ncl), t1 = (int)((int64_t)(cid + 1) * T / ncl);
@@ -270,10 +277,10 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     // ======================================================= tile walk + X producer (TMA)
     if (lane == 0 && n > 0) {
       const int Dv = p.ldx;
-      TileWalker tw, twp;  // box walker, L2-prefetch walker (4 tiles ahead)
-      tw.init(p, t0, t1);
-      twp.init(p, t0, t1);
+      TileWalker tw, twp;  // box walker, L2-prefetch walker (4 tiles ahead; set up after the first box
+                           // is requested: its index loads would otherwise delay tile 0 of a small launch)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
+      tw.init(p, t0, t1);
       auto prefetch_l2 = [&](int i) {
         if (i >= n) return;
         const TileMeta m = twp.meta();
@@ -282,7 +289,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
                      "r"((uint32_t)(m.nrows * Dv * 4) & ~15u)
                      : "memory");
       };
-      for (int i = 0; i < 4; ++i) prefetch_l2(i);
       for (int i = 0; i < n; ++i, tw.next()) {
         const TileMeta m = tw.meta();
         s_meta[i & 3] = m;  // released to the WORK warps by the X_FULL phase completions below
@@ -290,6 +296,11 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         if (i >= 1) mbar_wait(&bars[B_XEMPTY1], (i - 1) & 1);
         mbar_arrive_expect_tx(&bars[B_XFULL0], kXBoxBytes);
         tma_load_2d(sX, &tmap_x, 0, m.row0, &bars[B_XFULL0]);
+        if (i == 0) {
+          TRP(4);
+          twp.init(p, t0, t1);
+          for (int k = 0; k < 4; ++k) prefetch_l2(k);
+        }
         // box 1 (dims 32..63) after box 0 of this tile was released
         mbar_wait(&bars[B_XEMPTY0], i & 1);
         mbar_arrive_expect_tx(&bars[B_XFULL1], kXBoxBytes);
@@ -306,6 +317,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       const uint32_t idesc2 = idesc_f16_f32(kNF, kG, 1, 1);   // A = Z^T (SMEM, MN-major), B = P MN-major
       uint32_t folds = 0;
       mbar_wait(&bars[B_W_FULL], 0);
+      TRP(5);
       auto gemm1 = [&](int i) {
         mbar_wait(&bars[B_ZR_FULL], i & 1);
         if (i >= 1) mbar_wait(&bars[B_L_EMPTY], (i - 1) & 1);
@@ -400,24 +412,31 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       }
     };
     // S' quarter (lane = feature, columns 32h..) of a finished chunk -> the segment slot: stored by
-    // the segment's first chunk, added (red.global.add.v4.f32, same thread, program order) by the rest
+    // the segment's first chunk, added (red.global.add.v4.f32, same thread, program order) by the rest.
+    // The 32 x 32 block is transposed through this warp's own 4 KB of the P buffer (the bytes its
+    // P(i) stores overwrite next; GEMM2(i-1) has finished reading them) so that each global
+    // instruction covers 4 feature rows x 128 contiguous bytes instead of 32 rows x 16 bytes.
     auto fold = [&](int b, bool first) {
-      float *dst = p.slots + (size_t)seg_slot(cid, b) * kNF * p.Kp + (size_t)row * p.Kp + rank * kG + 32 * h;
+      float *base = p.slots + (size_t)seg_slot(cid, b) * kNF * p.Kp + (size_t)(32 * q) * p.Kp + rank * kG + 32 * h;
+      const uint32_t st0 = sP + (h >> 1) * kAtomBytes;
+      auto saddr = [&](int r, int j) {  // 16-byte chunk j (columns 4j..4j+3) of local row r
+        return st0 + (j >= 4 ? (uint32_t)kOpBytes : 0u) + sw_off(32 * q + r, 4 * (h & 1) + (j & 3));
+      };
       uint32_t v[32];
       tmem_ld32(tmem + kTS + lane_base + 32 * h, v);
       tmem_ld_wait(v);
-      if (first) {
-        float4 *d4 = reinterpret_cast<float4 *>(dst);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
-                              __uint_as_float(v[4 * j + 3]));
-      } else {
+      for (int j = 0; j < 8; ++j) sts128(saddr(lane, j), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          red_add_v4(dst + 4 * j, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                     __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+      for (int it = 0; it < 8; ++it) {
+        const int r = 4 * it + (lane >> 3), j = lane & 7;
+        const float4 x = *reinterpret_cast<const float4 *>(smem + (saddr(r, j) - sbase));
+        float *dst = base + (size_t)r * p.Kp + 4 * j;
+        if (first) *reinterpret_cast<float4 *>(dst) = x;
+        else red_add_v4(dst, x.x, x.y, x.z, x.w);
       }
+      __syncwarp();  // the P(i) stores of this warp reuse the staging bytes
     };
 
     float s0acc[32];
@@ -581,14 +600,18 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     }
     if (n > 0) {  // last chunk
       work_wait(&bars[B_G2_DONE], (n - 1) & 1);
+      if (warp == 0 && lane == 0) TRP(6);
       fold(prev_b, chunk_seg_first);
+      if (warp == 0 && lane == 0) TRP(7);
     }
   }
 
   // ---------------- teardown
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) TRP(8);
   cluster_sync();
+  if (tid == 0) TRP(9);
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
