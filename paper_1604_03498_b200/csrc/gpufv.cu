@@ -329,6 +329,7 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
                      const float *sg, unsigned flags, void *ws) {
   (void)mu; (void)sg;
   FinParams f;
+  f.trace = g_trace;
   f.slots = (const float *)at(ws, L.slots);
   f.s0slots = (const float *)at(ws, L.s0slots);
   f.stats = nullptr;
@@ -393,6 +394,26 @@ fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStrea
     if (e != cudaSuccess) return fail(FV_ERR_CUDA, "k_finalize_img launch: %s", cudaGetErrorString(e));
     g_launches += 1;
     return cuda_check("k_finalize_img");
+  }
+  // a handful of narrow images straight after k_stats: 4x the blocks (k_finalize_lat)
+  const int64_t lat_grid = (int64_t)((K + kFinJ - 1) / kFinJ) * batch * kLatZ;
+  if (after_stats && f.slots && f.n_cls == 0 && K <= kImgK && D <= kDP && lat_grid <= sm_count() &&
+      ((K + kFinJ - 1) / kFinJ) * kLatZ <= kFinMaxParts) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((K + kFinJ - 1) / kFinJ, batch, kLatZ);
+    cfg.blockDim = dim3(kLatThreads, 1, 1);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FinParams fc = f;
+    fc.b_base = 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_finalize_lat, fc);
+    if (e != cudaSuccess) return fail(FV_ERR_CUDA, "k_finalize_lat launch: %s", cudaGetErrorString(e));
+    g_launches += 1;
+    return cuda_check("k_finalize_lat");
   }
   if (!after_stats && cudaMemsetAsync(f.counters, 0, (size_t)batch * 4, st) != cudaSuccess)
     return cuda_check("memset tickets");

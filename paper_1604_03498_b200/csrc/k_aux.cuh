@@ -253,7 +253,15 @@ struct FinParams {
   float *scores;              // batch x n_cls
   double *spart;              // batch x kFinMaxParts x n_cls: each block's partial dot products
   int n_cls;
+  long long *trace;           // debug (GPUFV_TRACE builds): globaltimer points of block 0, slots 7700..
 };
+
+#ifdef GPUFV_TRACE
+#define TRF(slot) do { if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) \
+    p.trace[7700 + (slot)] = ptx::globaltimer(); } while (0)
+#else
+#define TRF(slot) do { } while (0)
+#endif
 
 constexpr int kMaxCls = 32;     // classes of the fused linear scoring
 
@@ -457,7 +465,8 @@ __device__ __forceinline__ double fin_tile(const FinParams &p, int b, int j0, in
 // padding and discarded).  Segment i is segs[i], or cfirst + i when segs == nullptr.  The 256 threads
 // of the tile meet once on named barrier bar_id.  Per-accumulator summation order = fin_tile's:
 // bitwise the same result.
-__device__ __forceinline__ double fin_tile_seg(const FinParams &p, int b, int j0, int kb, int tid, int bar_id,
+template <int kSegs = 2>  // segments whose loads are in flight together
+__device__ __forceinline__ double fin_tile_seg(const FinParams &p, int b, int j0, int kb, int tid, int bar_id, int bar_n,
                                                float (*sU)[kDP + 1], float (*sV)[kDP + 1], const int *segs,
                                                int cfirst, int nseg, double N, double *sS0, int s0base) {
   const int jq = tid & 7, kr = (tid >> 3) + kb;
@@ -468,49 +477,51 @@ __device__ __forceinline__ double fin_tile_seg(const FinParams &p, int b, int j0
   for (int r = 0; r < kFinKR; ++r)
 #pragma unroll
     for (int e = 0; e < 4; ++e) S1[r][e] = S2[r][e] = 0.0;
-  for (int si = 0; si < nseg; si += 2) {
-    const bool two = si + 1 < nseg;
-    const int ca = segs ? segs[si] : cfirst + si, cb = two ? (segs ? segs[si + 1] : ca + 1) : ca;
-    const float *sa = p.slots + (size_t)seg_slot(ca, b) * seg_stride + jb;
-    const float *sb = p.slots + (size_t)seg_slot(cb, b) * seg_stride + jb;
-    float4 a1[kFinKR], a2[kFinKR], b1[kFinKR], b2[kFinKR];
-    float z0[2][4];
+  TRF(8);
+  for (int si = 0; si < nseg; si += kSegs) {
+    int cs[kSegs];
+    bool ok[kSegs];
+    float4 v1[kSegs][kFinKR], v2[kSegs][kFinKR];
+    float z0[kSegs][4];
 #pragma unroll
-    for (int r = 0; r < kFinKR; ++r) {
-      const size_t k = (size_t)(kr + 32 * r) * p.Kp, k2 = k + (size_t)p.dpad * p.Kp;
-      a1[r] = __ldcs(reinterpret_cast<const float4 *>(sa + k));
-      a2[r] = __ldcs(reinterpret_cast<const float4 *>(sa + k2));
-      if (two) {
-        b1[r] = __ldcs(reinterpret_cast<const float4 *>(sb + k));
-        b2[r] = __ldcs(reinterpret_cast<const float4 *>(sb + k2));
+    for (int u = 0; u < kSegs; ++u) {
+      ok[u] = u == 0 || si + u < nseg;  // segment si is always valid
+      cs[u] = ok[u] ? (segs ? segs[si + u] : cfirst + si + u) : cfirst;
+      if (ok[u]) {
+        const float *sl = p.slots + (size_t)seg_slot(cs[u], b) * seg_stride + jb;
+#pragma unroll
+        for (int r = 0; r < kFinKR; ++r) {
+          const size_t k = (size_t)(kr + 32 * r) * p.Kp, k2 = k + (size_t)p.dpad * p.Kp;
+          v1[u][r] = __ldcs(reinterpret_cast<const float4 *>(sl + k));
+          v2[u][r] = __ldcs(reinterpret_cast<const float4 *>(sl + k2));
+        }
       }
     }
     if (tid < 32) {  // S0 of Gaussian j0 + tid: 4 row-group partials per segment
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < kSegs; ++u)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (u == 0 || two) z0[u][q] = __ldcs(p.s0slots + ((size_t)seg_slot(u ? cb : ca, b) * 4 + q) * p.Kp + j0 + tid);
+          if (ok[u]) z0[u][q] = __ldcs(p.s0slots + ((size_t)seg_slot(cs[u], b) * 4 + q) * p.Kp + j0 + tid);
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
-        if (u == 0 || two)
+      for (int u = 0; u < kSegs; ++u)
+        if (ok[u])
 #pragma unroll
           for (int q = 0; q < 4; ++q) S0l += (double)z0[u][q];
     }
 #pragma unroll
-    for (int r = 0; r < kFinKR; ++r) {
-      S1[r][0] += (double)a1[r].x; S1[r][1] += (double)a1[r].y; S1[r][2] += (double)a1[r].z; S1[r][3] += (double)a1[r].w;
-      S2[r][0] += (double)a2[r].x; S2[r][1] += (double)a2[r].y; S2[r][2] += (double)a2[r].z; S2[r][3] += (double)a2[r].w;
-    }
-    if (two)
+    for (int u = 0; u < kSegs; ++u)
+      if (ok[u])
 #pragma unroll
-      for (int r = 0; r < kFinKR; ++r) {
-        S1[r][0] += (double)b1[r].x; S1[r][1] += (double)b1[r].y; S1[r][2] += (double)b1[r].z; S1[r][3] += (double)b1[r].w;
-        S2[r][0] += (double)b2[r].x; S2[r][1] += (double)b2[r].y; S2[r][2] += (double)b2[r].z; S2[r][3] += (double)b2[r].w;
-      }
+        for (int r = 0; r < kFinKR; ++r) {
+          S1[r][0] += (double)v1[u][r].x; S1[r][1] += (double)v1[u][r].y; S1[r][2] += (double)v1[u][r].z; S1[r][3] += (double)v1[u][r].w;
+          S2[r][0] += (double)v2[u][r].x; S2[r][1] += (double)v2[u][r].y; S2[r][2] += (double)v2[u][r].z; S2[r][3] += (double)v2[u][r].w;
+        }
   }
+  TRF(5);
   if (tid < 32) sS0[j0 + tid - s0base] = S0l * (1.0 / (double)kPScale);  // S0 was accumulated from P = gamma 2^14
-  ptx::named_bar_sync(bar_id, 256);  // the tile's S0
+  ptx::named_bar_sync(bar_id, bar_n);  // the tile's S0
+  TRF(6);
 #pragma unroll
   for (int e = 0; e < 4; ++e) S0[e] = sS0[jb + e - s0base];
   double fu[4], fv[4];
@@ -575,7 +586,9 @@ __device__ __forceinline__ double fin_tile_seg(const FinParams &p, int b, int j0
 // path).  For large batches the last-block variant wins (waiting blocks would hold slots).
 template <bool kScore, bool kSync>  // kScore = false: the plain encode (no scoring code compiled in)
 __global__ void __launch_bounds__(256, 2) k_finalize(const FinParams p) {
+  TRF(0);
   ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
+  TRF(1);
   __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
   __shared__ double s_red[8];
   __shared__ float s_dot[8][kMaxCls];
@@ -588,12 +601,13 @@ __global__ void __launch_bounds__(256, 2) k_finalize(const FinParams p) {
   if (p.slots && p.tile_start[p.batch] >= (int64_t)p.ncl) {  // every cluster non-empty: segments = cown range
     __shared__ double s_S0[kFinJ];
     const int lo = p.cown[2 * b], hi = p.cown[2 * b + 1];
-    ss = fin_tile_seg(p, b, j0, kb, tid, 1, sU, sV, nullptr, lo, hi - lo + 1,
+    ss = fin_tile_seg(p, b, j0, kb, tid, 1, 256, sU, sV, nullptr, lo, hi - lo + 1,
                       (double)(p.offsets[b + 1] - p.offsets[b]), s_S0, j0);
   } else {
     ss = fin_tile(p, b, j0, kb, tid, sU, sV);
   }
   __syncthreads();
+  TRF(2);
   const int part = blockIdx.z * gridDim.x + blockIdx.x, nparts = gridDim.x * gridDim.z;
   if (!kSync && (!kScore || p.out)) {
     float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D + kb;
@@ -659,6 +673,7 @@ __global__ void __launch_bounds__(256, 2) k_finalize(const FinParams p) {
         __threadfence();
       }
       __syncthreads();
+      TRF(3);
       double n2 = 0.0;  // fixed-order sum of the parts: the same bits in every block
       if (l2)
         for (int k = 0; k < nparts; ++k) n2 += __ldcg(p.norm2 + (size_t)b * kFinMaxParts + k);
@@ -678,6 +693,7 @@ __global__ void __launch_bounds__(256, 2) k_finalize(const FinParams p) {
         o[KD + (size_t)r * p.D + k] = sV[r][k] * sc;
       }
     }
+    TRF(4);
     return;
   }
   if (!kScore && !l2) return;
@@ -794,7 +810,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
                             : (p.slots ? (double)(p.offsets[b + 1] - p.offsets[b]) : 0.0);
     double ss = 0.0;
     for (int t = grp; t < ntiles; t += kImgThreads / 256)
-      ss += use_list ? fin_tile_seg(p, b, t * kFinJ, 0, gt, 1 + grp, iU + t * kFinJ, iV + t * kFinJ,
+      ss += use_list ? fin_tile_seg(p, b, t * kFinJ, 0, gt, 1 + grp, 256, iU + t * kFinJ, iV + t * kFinJ,
                                     direct ? nullptr : s_segs, cfirst, nseg, N, s_S0, 0)
                      : fin_tile(p, b, t * kFinJ, 0, gt, iU + t * kFinJ, iV + t * kFinJ);
 #pragma unroll
@@ -852,6 +868,80 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
     if (direct && tid == 0) ptx::cp_async_wait_all();
     __syncthreads();  // the next image overwrites the shared image, s_red, s_S0 and the segment list
   }
+}
+
+// Latency path (a handful of images, K <= 256, D <= 64, slots): the tile-parallel finalize with
+// 4x the blocks — block (x, b, z) takes Gaussians 32x .. +31 and dims 8z .. +7 and 32 + 8z .. +7 with
+// 64 threads (fin_tile_seg's thread layout with kr = tid / 8 < 8) — because one image's segment
+// reads are bound by the per-SM L2 -> SM bandwidth of the few SMs that hold its blocks (a 5,000-
+// descriptor frame over 10 segments pulls 1.3 MB: ~7 us on 8 SMs).  All blocks are co-resident
+// (grid <= SMs): each publishes its partial sum of squares, waits for its image's siblings and writes
+// its sub-tile once, scaled (as k_finalize<.., kSync>).
+constexpr int kLatThreads = 64;
+constexpr int kLatZ = 4;     // dim slices per 64 dims
+constexpr int kLatSegs = 8;  // segment loads in flight per thread (the chain is L2-latency bound)
+__global__ void __launch_bounds__(kLatThreads) k_finalize_lat(const FinParams p) {
+  ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
+  TRF(1);
+  __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
+  __shared__ double s_S0[kFinJ];
+  __shared__ double s_red[kLatThreads / 32];
+  __shared__ int s_segs[kImgMaxSeg];
+  __shared__ int s_nseg;
+  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x;
+  const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), kb = 8 * (int)blockIdx.z;
+  const bool direct = p.tile_start[p.batch] >= (int64_t)p.ncl;
+  if (!direct && tid == 0) {  // some cluster owns no tile: scan for the image's non-empty segments
+    const int ft = (int)p.tile_start[b], lt = (int)p.tile_start[b + 1];
+    int ns = 0;
+    for (int c = p.cown[2 * b]; c <= p.cown[2 * b + 1] && ns < kImgMaxSeg; ++c) {
+      const int st = p.cstart[c], en = p.cstart[c + 1];
+      if ((st > ft ? st : ft) < (en < lt ? en : lt)) s_segs[ns++] = c;
+    }
+    s_nseg = ns;
+  }
+  __syncthreads();
+  const int lo = p.cown[2 * b], hi = p.cown[2 * b + 1];
+  double ss = fin_tile_seg<kLatSegs>(p, b, j0, kb, tid, 1, kLatThreads, sU, sV, direct ? nullptr : s_segs, lo,
+                           direct ? hi - lo + 1 : s_nseg, (double)(p.offsets[b + 1] - p.offsets[b]), s_S0, j0);
+  TRF(2);
+  const int part = blockIdx.z * gridDim.x + blockIdx.x, nparts = gridDim.x * gridDim.z;
+  const bool l2 = p.mode != 2;
+  float sc = 1.f;
+  if (l2) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if ((tid & 31) == 0) s_red[tid >> 5] = ss;
+    __syncthreads();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < kLatThreads / 32; ++w) tot += s_red[w];
+      p.norm2[(size_t)b * kFinMaxParts + part] = tot;  // own slot
+      __threadfence();
+      unsigned *ctr = p.counters + b;
+      atomicAdd(ctr, 1u);
+      while (atomicAdd(ctr, 0u) < (unsigned)nparts) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
+    TRF(3);
+    double n2 = 0.0;  // fixed-order sum of the parts: the same bits in every block
+    for (int k = 0; k < nparts; ++k) n2 += __ldcg(p.norm2 + (size_t)b * kFinMaxParts + k);
+    if (n2 > 0.0) sc = (float)(1.0 / sqrt(n2));
+  } else {
+    __syncthreads();
+  }
+  // this block's (nj x 16) sub-tile: thread -> (Gaussian r, 8-dim strip half, dim)
+  const int KD = p.K * p.D;
+  float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D;
+  for (int t = tid; t < nj * 16; t += kLatThreads) {
+    const int r = t >> 4, c = t & 15, k = kb + (c & 7) + 32 * (c >> 3);
+    if (k < p.D) {
+      o[(size_t)r * p.D + k] = sU[r][k - kb] * sc;
+      o[KD + (size_t)r * p.D + k] = sV[r][k - kb] * sc;
+    }
+  }
+  TRF(4);
 }
 
 // a6 only: slots -> fp64 stats [N, S0, S1, S2] about c (reading A19).  Same grid as k_finalize.

@@ -235,6 +235,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
 
   if (tid == 0) TRP(0);
+#ifdef GPUFV_TRACE
+  if (p.trace && cid == 0 && rank == 0 && tid == 0) p.trace[7720] = ptx::globaltimer();
+#endif
   // ---------------- setup
   {
     for (int i = tid; i < kG; i += kThreads2) s_bias[i] = p.bias[rank * kG + i];
@@ -612,6 +615,10 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   if (tid == 0) TRP(8);
   cluster_sync();
   if (tid == 0) TRP(9);
+#ifdef GPUFV_TRACE
+  if (p.trace && cid == 0 && rank == 0 && tid == 0) p.trace[7721] = ptx::globaltimer();
+  if (p.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long *>(p.trace + 7722), (unsigned long long)ptx::globaltimer());
+#endif
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 

@@ -61,3 +61,13 @@ work = t[1024:1024 + 64 * 4 * 16].reshape(64, 4, 16)
 for i in range(64):
     if work[i, 0, 0]:
         print(f"  tile {i}: WORK slot 0 (L ready) {work[i, 0, 0] - t0:8d}   P write done (slot 9) {work[i, 0, 9] - t0:8d}")
+G = t[7700:7723]
+g0 = G[20]
+print("global timeline (ns from k_stats CTA 0 entry, %globaltimer):")
+for k, name in [(20, "k_stats CTA 0 entry"), (21, "k_stats CTA 0 end"), (22, "k_stats last CTA end"),
+                (0, "k_finalize block 0 entry"), (1, "k_finalize griddep_wait returned"),
+                (8, "k_finalize segment loop start"), (5, "k_finalize segment loads summed"),
+                (6, "k_finalize S0 barrier passed"), (2, "k_finalize tile computed"), (3, "k_finalize image norm known (all blocks)"),
+                (4, "k_finalize block 0 end")]:
+    if G[k]:
+        print(f"  {name:42s} {G[k] - g0:8d}")
