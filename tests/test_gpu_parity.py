@@ -152,6 +152,37 @@ def test_mostly_empty_batch_segment_scan(fv, batch):
             assert rel_l2(out[b], ref[b]) <= FV_RTOL, (b, n, rel_l2(out[b], ref[b]))
 
 
+_SCAN_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import fvgen, oracle, paper_1604_03498_b200 as fv
+gmm_np = fvgen.make_gmm(256, 64, seed=1604)
+counts = [0, 1, 0, 3]
+X, off = fvgen.make_batch(gmm_np, counts, seed_base=808)
+out = fv.encode_batched(torch.from_numpy(X).cuda(), torch.from_numpy(off).cuda(), fv.GMM(*gmm_np),
+                        threshold=1e-6).cpu().numpy()
+ref = oracle.encode_batched(X, off, *gmm_np, threshold=1e-6)
+err = max(np.linalg.norm(out[b] - ref[b]) / np.linalg.norm(ref[b]) for b in (1, 3))
+assert np.all(out[0] == 0) and np.all(out[2] == 0)
+print(err)
+"""
+
+
+def test_latency_finalize_segment_scan_subprocess(fv):
+    """k_finalize_lat (a few narrow images) on a launch with more clusters than tiles: GPUFV_MIN_TILES=1
+    (read once per process, hence the subprocess) gives 4 clusters for 2 tiles, so the kernel scans
+    for the non-empty segments instead of using the owner-table range."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GPUFV_MIN_TILES="1")
+    r = subprocess.run([sys.executable, "-c", _SCAN_SCRIPT, root], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= FV_RTOL
+
+
 def test_batched_equals_per_image_and_deterministic(fv):
     gmm_np = fvgen.make_gmm(256, 64, seed=1604)
     X, off = fvgen.make_batch(gmm_np, [3000, 257, 4096], seed_base=5)
