@@ -2,7 +2,7 @@
 // layout, launches.  No allocation, no synchronisation (except fv_encode_batched_host, which must
 // return host results), no CPU fallback: every step of the path runs in the kernels below.
 // Experiment knobs (environment, read once per process; defaults are the measured best):
-//   GPUFV_MIN_TILES=<n>   minimum tiles per cluster for small launches (default 4)
+//   GPUFV_MIN_TILES=<n>   minimum tiles per cluster for small launches (default 3)
 //   GPUFV_FIN_TILES=1     force the tile-parallel finalize for large batches (default: k_finalize_img)
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -65,7 +65,7 @@ int sm_count() {
 
 // Tile family: D <= 64 -> k_stats (128 Gaussians per CTA, cluster <= 4); 64 < D <= 128 -> k_stats_w
 // (64 Gaussians per CTA, cluster <= 8).  K <= 512 for both.
-constexpr int kMinTilesPerClusterDefault = 4;
+constexpr int kMinTilesPerClusterDefault = 3;
 constexpr int kMaxSegPerImage = 26;
 // GPUFV_MIN_TILES overrides it (latency experiments only); read once per process
 int min_tiles_per_cluster() {
