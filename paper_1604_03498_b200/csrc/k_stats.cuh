@@ -313,12 +313,18 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     }
   } else if (warp == kWarpMma) {
     // ======================================================= MMA issuer
-    if (lane == 0 && n > 0) {
+    if (n > 0) {  // the whole warp, converged; one elected lane issues (ptx::*_w)
       TileWalker tw;
       tw.init(p, t0, t1);
       const uint32_t idesc1 = idesc_f16_f32(128, kG, 0, 0);   // A = Zr (TMEM, K-major), B = W' K-major
       const uint32_t idesc2 = idesc_f16_f32(kNF, kG, 1, 1);   // A = Z^T (SMEM, MN-major), B = P MN-major
       uint32_t folds = 0;
+      // operand descriptors built once: per UMMA only a compile-time offset (>> 4, into the 14-bit
+      // start-address field; every shared address is < 2^18, so the field never carries) is added —
+      // the issuing thread shares its sub-partition with four WORK warps, so its instruction count per
+      // UMMA matters
+      const uint64_t dW = desc_sw128(sW, 16, 1024);
+      const uint64_t dZ = desc_sw128(sZ, kAtomBytes, 1024), dP = desc_sw128(sP, kAtomBytes, 1024);
       mbar_wait(&bars[B_W_FULL], 0);
       TRP(5);
       auto gemm1 = [&](int i) {
@@ -329,14 +335,14 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
 #pragma unroll
         for (int s = 0; s < 3; ++s) {  // cross terms first, hi.hi last (truncating accumulator)
           const uint32_t za = zr + (s == 1 ? 64 : 0);          // hi, lo, hi
-          const uint32_t wb = sW + (s == 0 ? kOpBytes : 0);    // lo, hi, hi
+          const uint32_t wb = (s == 0 ? kOpBytes : 0);         // lo, hi, hi
 #pragma unroll
           for (int kk = 0; kk < kNF / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
-            mma_f16_ts(tmem + kTL, za + kk * 8, desc_sw128(wb + off, 16, 1024), idesc1, (s | kk) != 0);
+            const uint32_t off = wb + (kk >> 2) * kAtomBytes + (kk & 3) * 32;
+            mma_f16_ts_w(tmem + kTL, za + kk * 8, dW + (off >> 4), idesc1, (s | kk) != 0);
           }
         }
-        mma_commit(&bars[B_G1_DONE]);
+        mma_commit_w(&bars[B_G1_DONE]);
       };
       auto gemm2 = [&](int i, bool chunk_first) {
         mbar_wait(&bars[B_P_FULL], i & 1);  // P(i) and Z(i) in shared memory
@@ -344,16 +350,16 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
-          const uint32_t za = sZ + (s == 1 ? kOpBytes : 0);    // hi, lo, hi
-          const uint32_t pb = sP + (s == 0 ? kOpBytes : 0);    // lo, hi, hi
+          const uint32_t za = (s == 1 ? kOpBytes : 0);         // hi, lo, hi
+          const uint32_t pb = (s == 0 ? kOpBytes : 0);         // lo, hi, hi
 #pragma unroll
           for (int kk = 0; kk < kTileM / 16; ++kk) {
             const uint32_t off = kk * 2048;  // 16 descriptor rows x 128 B
-            mma_f16_ss(tmem + kTS, desc_sw128(za + off, kAtomBytes, 1024), desc_sw128(pb + off, kAtomBytes, 1024),
-                       idesc2, (chunk_first && s == 0 && kk == 0) ? 0u : 1u);
+            mma_f16_ss_w(tmem + kTS, dZ + ((za + off) >> 4), dP + ((pb + off) >> 4), idesc2,
+                       (chunk_first && s == 0 && kk == 0) ? 0u : 1u);
           }
         }
-        mma_commit(&bars[B_G2_DONE]);
+        mma_commit_w(&bars[B_G2_DONE]);
       };
       gemm1(0);
       for (int i = 0; i < n; ++i, tw.next()) {
