@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
     }
   } else if (warp == kWarpMma) {
     // ======================================================= MMA issuer
-    if (lane == 0 && n > 0) {
+    if (n > 0) {  // the whole warp, converged; one elected lane issues (ptx::*_w)
       TileWalker tw;
       tw.init(p, t0, t1);
       const uint32_t idesc1 = idesc_f16_f32(128, kGW, 0, 0);  // A = Zr (TMEM, K-major), B = W' K-major
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         for (int kk = 0; kk < kNF / 16; ++kk) {
           if (!((mask >> kk) & 1u)) continue;
           const uint32_t off = (kk >> 2) * (kGW * 128) + (kk & 3) * 32;
-          mma_f16_ts(tmem + kWTL, za + kk * 8, desc_sw128(wb + off, 16, 1024), idesc1, (first && kk == 0) ? 0u : 1u);
+          mma_f16_ts_w(tmem + kWTL, za + kk * 8, desc_sw128(wb + off, 16, 1024), idesc1, (first && kk == 0) ? 0u : 1u);
         }
       };
       // GEMM1 in two parts so half a's cross terms run while half b is still being converted; all
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         g1(1, 1);
         g1(2, 0);
         g1(2, 1);
-        mma_commit(&bars[W_G1_DONE]);
+        mma_commit_w(&bars[W_G1_DONE]);
       };
       auto gemm1 = [&](int i) { gemm1a(i); gemm1b(i); };
       auto gemm2 = [&](int hf, bool chunk_first) {  // S'_hf (+)= Z_hf^T P over the tile's 128 rows
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
 #pragma unroll
           for (int kk = 0; kk < kTileM / 16; ++kk) {
             const uint32_t off = kk * 2048;  // 16 descriptor rows x 128 B
-            mma_f16_ss(tmem + kWTS + kGW * hf, desc_sw128(za + off, kAtomBytes, 1024),
+            mma_f16_ss_w(tmem + kWTS + kGW * hf, desc_sw128(za + off, kAtomBytes, 1024),
                        desc_sw128(pb + off, kAtomBytes, 1024), idesc2, (chunk_first && s == 0 && kk == 0) ? 0u : 1u);
           }
         }
@@ -210,13 +210,13 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         if (chunk_first && i > 0) { mbar_wait(&bars[W_FOLD_DONE], folds & 1); ++folds; }
         TR(10);
         gemm2(0, chunk_first);
-        mma_commit(&bars[W_G2A_DONE]);
+        mma_commit_w(&bars[W_G2A_DONE]);
         TR(11);
         if (i + 1 < n) gemm1a(i + 1);        // Zr(i+1) half a is converted before Z_b(i) is copied
         mbar_wait(&bars[W_ZB_FULL], i & 1);  // Z_b(i)
         TR(12);
         gemm2(1, chunk_first);
-        mma_commit(&bars[W_G2_DONE]);
+        mma_commit_w(&bars[W_G2_DONE]);
         TR(13);
         if (i + 1 < n) gemm1b(i + 1);
         TR(14);
