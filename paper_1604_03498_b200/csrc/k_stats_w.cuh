@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
     }
   } else {
     // ======================================================= WORK warps
-    const int q = warp & 3, h = warp >> 2;  // TMEM lanes 32q.. ; Gaussian quarter h (16 columns)
+    const int ww = warp - kWarpWork0;       // WORK warp index 0..15
+    const int q = warp & 3, h = ww >> 2;    // TMEM lanes 32q.. (physical warp % 4); Gaussian quarter h (16 columns)
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
     const int row = 32 * q + lane;  // descriptor row of Zr / L / P / Z; feature (of a half) of S'
     const float thr = p.threshold * kPScale;
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       if (C > 1) {
         const int par = i & 1;
         float2 *xb = s_xchg + par * (kMaxCW * kTileM);
-        if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&bars[W_XCHG0 + par], (C - 1) * kTileM * 8);
+        if (ww == 0 && lane == 0) mbar_arrive_expect_tx(&bars[W_XCHG0 + par], (C - 1) * kTileM * 8);
         if (h == 0) {
           const uint32_t my = smem_u32(&xb[rank * kTileM + row]);
           const uint32_t mybar = smem_u32(&bars[W_XCHG0 + par]);
