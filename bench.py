@@ -8,7 +8,15 @@ path.  value = descriptors/s over all ranks (max-over-ranks device time).  Input
 larger than the 126 MB L2, so no flush between steps is needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--frames F] [--impl reference]
-  (N > 1: torchrun --nproc-per-node N ... bench.py --gpus N)
+  (N > 1: torchrun --nproc-per-node N ... bench.py --gpus N; without torchrun, --gpus N > 1 launches the
+   N ranks itself through torch.distributed.run)
+
+Every workload partitions through paper_1604_03498_b200.dist (FrameShard / encode_frames_sharded for the
+frame streams, encode_descriptor_sharded for C5, em_step_sharded for EM), and every rank draws its slice
+of ONE fixed global set (fvgen.make_frames(start=..., total=...)), so the N-GPU result is the same set's
+result whatever N is.  Every rank self-checks its outputs before timing without the oracle (finite, unit
+norm, range flags clear, sum_j S0_j = N; for C5 the full set's FV against the oracle-written
+tests/golden/large_c5.npz); the oracle itself runs only in the cpu_baseline leg (rank 0, N = 1).
 """
 from __future__ import annotations
 
@@ -51,8 +59,22 @@ def parse():
     ap.add_argument("--workload", default="c4", choices=["c4", "c5", "em", "embed"],
                     help="c4: frame-sharded stream (default, the metric's config); c5: one 10M x 128 set, K=512, "
                          "descriptor-sharded with an NCCL all-reduce of the fp64 statistics")
+    ap.add_argument("--no-legs", action="store_true", help="skip the C1 / C3 legs of the default run")
     ap.add_argument("--c5-n", type=int, default=10_000_000, help="C5 set size (all ranks together)")
     return ap.parse_args()
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: run this script under torch.distributed.run with N
+    ranks on this node (rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -62,13 +84,40 @@ def dist_env():
     return rank, world, local
 
 
-def make_stream(frames: int, rank: int):
-    """C4-shaped synthetic stream for this rank (fvgen recipe, float32 blocks of 64 frames, seed
-    1604 + 20000 + rank * 1_000_003 + first frame of the block)."""
+def make_stream(frames: int, rank: int = 0, world: int = 1):
+    """C4-shaped synthetic stream: one global stream of world x frames frames (fvgen recipe, float32 blocks
+    of 64 frames seeded 1604 + 20000 + first frame of the block); this rank's rows are its FrameShard's
+    frames [lo, hi) = shard_ranges(world x frames, world)[rank].  Returns (gmm, X rows of this rank,
+    global frame offsets, the FrameShard's (lo, hi))."""
     gmm = fvgen.make_gmm(K, D, seed=fvgen.SEED_GMM)
-    X = fvgen.make_frames(gmm, frames, PER_FRAME, seed=1604 + 20000 + rank * 1_000_003)
-    offsets = np.arange(frames + 1, dtype=np.int64) * PER_FRAME
-    return gmm, X, offsets
+    total = world * frames
+    lo, hi = rank * total // world, (rank + 1) * total // world
+    X = fvgen.make_frames(gmm, hi - lo, PER_FRAME, seed=1604 + 20000, start=lo, total=total)
+    offsets = np.arange(total + 1, dtype=np.int64) * PER_FRAME
+    return gmm, X, offsets, (lo, hi)
+
+
+def peak_for(timed_s: float):
+    """(peak TFLOP/s, which) for the dominant kernel: the burst cuBLAS bf16 figure when the whole timed
+    region is short (< 1 s: the clocks stay at their maximum), else the sustained one (kind::f16 runs at
+    the bf16 rate).  MEASURED_PEAKS.json, else B200_PROFILING.md's fallback."""
+    pk = load_peaks()
+    burst = float(pk.get("bf16_tflops", 1590.0))
+    sus = float(pk.get("bf16_tflops_sustained", 1400.0))
+    src = "MEASURED_PEAKS.json" if "bf16_tflops" in pk else "B200_PROFILING.md fallback"
+    if timed_s < 1.0:
+        return burst, sus, f"burst: {src} bf16_tflops (timed region {timed_s:.2f} s < 1 s)"
+    return sus, burst, f"sustained: {src} bf16_tflops_sustained (timed region {timed_s:.2f} s >= 1 s)"
+
+
+def self_check_fvs(out, label):
+    """Oracle-free checks every rank runs before timing: finite, unit L2 norm (improved FV)."""
+    import torch
+    if not bool(torch.isfinite(out).all()):
+        raise SystemExit(f"{label}: non-finite FV before timing")
+    nrm = out.double().norm(dim=-1)
+    if float((nrm - 1.0).abs().max()) > 1e-4:
+        raise SystemExit(f"{label}: FV norms off unit before timing")
 
 
 class ClockSampler:
@@ -202,7 +251,7 @@ def run_reference(args, rank, world):
     paper-only tier); rank 0 alone runs it."""
     if rank != 0:
         return
-    gmm, X, _ = make_stream(min(args.frames, 4096), 0)
+    gmm, X, _, _ = make_stream(min(args.frames, 4096))
     import oracle
     threads = oracle.max_threads()
     n = int(max(1, min(args.frames, round(threads * max(1.0, args.cpu_seconds / max(1, args.steps))))))
@@ -237,14 +286,120 @@ def load_peaks():
         return {}
 
 
-def tensor_peak():
-    """(TFLOP/s, source) for a kernel timed inside a long step: MEASURED_PEAKS.json's sustained cuBLAS
-    bf16 figure (kind::f16 runs at the bf16 rate), else the profiling guide's stated fallback."""
-    pk = load_peaks()
-    if "bf16_tflops_sustained" in pk:
-        return float(pk["bf16_tflops_sustained"]), "of measured: MEASURED_PEAKS.json bf16_tflops_sustained (kind::f16 = bf16 rate)"
-    return 1400.0, ("of fallback: MEASURED_PEAKS.json absent; B200_PROFILING.md fallback 1.59 PF burst, "
-                    "~1.4 PF sustained under the power cap (kind::f16 = bf16 rate)")
+def run_legs(fv, gmm, gmm_np, dev, stream, rank, world):
+    """The other BASELINE configs as legs of the default run (device-timed, CUDA events, max over ranks):
+    C3 (configs[2]): a VOC2007-shaped ragged batch of 256 images x round(20000 U(0.75, 1.25)) descriptors
+       per rank, tau = 1e-6, one fv_encode_batched call (this batch size takes the whole-image finalize);
+       the rank's images are its dist.partition_images share of a 256 x world global batch.
+    C1 (configs[0]): one 1000-descriptor image, K = 16, exact posteriors: call latency, eager and graph."""
+    import torch
+    from paper_1604_03498_b200 import dist as fvdist
+    legs = {}
+    cfg = fvgen.CONFIGS["C3"]
+    counts_all = fvgen.voc_counts(cfg["B"] * world, seed=cfg["seed_data"], mean=cfg["mean"])
+    mine = fvdist.partition_images(counts_all, world)[rank]
+    counts = counts_all[mine]
+    offs = np.zeros(len(counts) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(counts)
+    Xc = np.empty((int(offs[-1]), D), dtype=np.float32)
+    for i, b in enumerate(mine):
+        Xc[offs[i]:offs[i + 1]] = fvgen.make_descriptors(gmm_np, int(counts[i]), cfg["seed_data"] + int(b))
+    Xcd, offcd = torch.from_numpy(Xc).to(dev), torch.from_numpy(offs).to(dev)
+    ws3 = fv.Workspace(device=dev)
+    ws3.ensure(fv.workspace_bytes(Xc.shape[0], len(counts), K, D))
+    fv.gmm_prepare(gmm, ws3)
+    o3 = torch.empty(len(counts), 2 * K * D, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        fv.encode_batched(Xcd, offcd, gmm, threshold=TAU, ws=ws3, prepared=True, out=o3)
+    torch.cuda.synchronize(dev)
+    self_check_fvs(o3, "C3")
+    reps = 10
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fv.encode_batched(Xcd, offcd, gmm, threshold=TAU, ws=ws3, prepared=True, out=o3)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms3 = a.elapsed_time(b) / reps
+    if world > 1:
+        t = torch.tensor([ms3], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms3 = float(t.item())
+    legs["c3"] = {"value": int(offs[-1]) * world / (ms3 * 1e-3), "unit": UNIT, "ms_per_batch": ms3,
+                  "images_per_rank": len(counts), "descriptors_per_rank": int(offs[-1]),
+                  "workload": f"C3 VOC2007-shaped batch: {len(counts)} images x ~{cfg['mean']} descriptors (ragged) "
+                              f"per rank, K={K}, D={D}, tau={TAU}, one fv_encode_batched call; {reps} calls timed"}
+    del Xcd, ws3, o3
+    c1 = fvgen.CONFIGS["C1"]
+    g1np = fvgen.make_gmm(c1["K"], c1["D"], seed=c1["seed_gmm"])
+    x1 = torch.from_numpy(fvgen.make_descriptors(g1np, c1["counts"][0], seed=c1["seed_data"])).to(dev)
+    g1 = fv.GMM(*g1np, device=dev)
+    ws1 = fv.Workspace(device=dev)
+    ws1.ensure(fv.workspace_bytes(x1.shape[0], 1, c1["K"], c1["D"]))
+    fv.gmm_prepare(g1, ws1)
+    o1 = torch.empty(2 * c1["K"] * c1["D"], dtype=torch.float32, device=dev)
+
+    def one():
+        fv.encode(x1, g1, ws=ws1, prepared=True, out=o1)
+
+    legs["c1"] = {"eager_us": latency_us(one, dev, stream)}
+    legs["c1"]["graph_us"] = graph_latency_us(one, dev, stream)
+    legs["c1"]["workload"] = f"C1: one image, {c1['counts'][0]} descriptors, K={c1['K']}, D={c1['D']}, exact"
+    return legs
+
+
+def latency_us(fn, dev, stream, reps=200):
+    import torch
+    for _ in range(10):
+        fn()
+    es = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in es:
+        a.record(stream); fn(); b.record(stream)
+    torch.cuda.synchronize(dev)
+    us = sorted(1e3 * a.elapsed_time(b) for a, b in es)
+    return {"p50": us[len(us) // 2], "p99": us[int(0.99 * (len(us) - 1))]}
+
+
+def graph_latency_us(fn, dev, stream):
+    import torch
+    try:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(stream)
+        with torch.cuda.stream(s):
+            fn()
+            torch.cuda.synchronize(dev)
+            with torch.cuda.graph(g, stream=s):
+                fn()
+        stream.wait_stream(s)
+        return latency_us(g.replay, dev, stream)
+    except Exception as e:  # noqa: BLE001
+        return f"capture failed: {e}"
+
+
+def stress_errors(fv, dev):
+    """The survey's stress generators (not the acceptance set) against the oracle, on one
+    5000-descriptor frame each (cpu_baseline leg, rank 0, N = 1): max |gamma error| (exact posteriors)
+    and FV rel-L2 (exact and tau = 1e-6); range flags are reported too."""
+    import torch
+    import oracle
+    res = {}
+    for name, kw in (("f0.15", dict(f=0.15)), ("peaked", dict(kind="peaked"))):
+        g_np = fvgen.make_gmm(K, D, seed=1604, **kw)
+        x = fvgen.make_descriptors(g_np, PER_FRAME, seed=1604 + 1000)
+        g = fv.GMM(*g_np, device=dev)
+        xd = torch.from_numpy(x).to(dev)
+        gam = fv.posteriors(xd, g).cpu().numpy()
+        r = {"gamma_max_abs_err": float(np.abs(gam - oracle.posteriors(x, *g_np)).max())}
+        for tau in (0.0, TAU):
+            ws = fv.Workspace(device=dev)
+            out = fv.encode(xd, g, threshold=tau, ws=ws).cpu().numpy().astype(np.float64)
+            ref = oracle.encode(x, *g_np, threshold=tau)
+            r[f"fv_rel_l2_tau{tau:g}"] = float(np.linalg.norm(out - ref) / np.linalg.norm(ref))
+            r[f"range_flag_tau{tau:g}"] = int(fv.range_flags(ws, PER_FRAME, 1, g).item())
+        res[name] = r
+    res["tolerance"] = {"gamma_abs": 1e-5, "fv_rel_l2": 1e-4, "note": "stress sets are reported, not gated"}
+    return res
 
 
 def run_c5(args, rank, world, local):
@@ -264,10 +419,12 @@ def run_c5(args, rank, world, local):
     from paper_1604_03498_b200 import dist as fvdist
     cfg = fvgen.CONFIGS["C5"]
     K5, D5, frame = cfg["K"], cfg["D"], 5000
-    lo, hi = fvdist.shard_ranges(args.c5_n // frame, world)[rank]
+    nfr = args.c5_n // frame
+    lo, hi = fvdist.shard_ranges(nfr, world)[rank]
     n = (hi - lo) * frame
     gmm_np = fvgen.make_gmm(K5, D5, seed=cfg["seed_gmm"])
-    X = fvgen.make_frames(gmm_np, hi - lo, frame, seed=cfg["seed_data"] + rank * 1_000_003).reshape(n, D5)
+    # this rank's contiguous rows of the ONE global set (the set tests/golden/large_c5.npz holds)
+    X = fvgen.make_frames(gmm_np, hi - lo, frame, seed=cfg["seed_data"], start=lo, total=nfr).reshape(n, D5)
     gmm = fv.GMM(*gmm_np, device=dev)
     Xd = torch.from_numpy(X).to(dev)
     offd = torch.tensor([0, n], dtype=torch.int64, device=dev)
@@ -279,28 +436,44 @@ def run_c5(args, rank, world, local):
     stream = torch.cuda.current_stream(dev)
     launches = [0]
 
-    def step():
-        fv.stats_batched(Xd, offd, gmm, ws=ws, prepared=True, out=st)
+    def stats_fn(Xs):
+        fv.stats_batched(Xs, offd, gmm, ws=ws, prepared=True, out=st)
         launches[0] = fv.last_launch_count()
-        if world > 1:
-            torch.distributed.all_reduce(st, op=torch.distributed.ReduceOp.SUM)  # a8
-        fv.finalize(st, gmm, ws=ws, prepared=True, out=out)
-        launches[0] += fv.last_launch_count()
+        return st
 
-    step()
+    def finalize_fn(s):
+        fv.finalize(s, gmm, ws=ws, prepared=True, out=out)
+        launches[0] += fv.last_launch_count()
+        return out
+
+    def step():  # a2-a6 on this rank's shard, a8 all-reduce (world > 1), a7 (dist.encode_descriptor_sharded)
+        return fvdist.encode_descriptor_sharded(Xd, gmm, stats_fn=stats_fn, finalize_fn=finalize_fn,
+                                                return_stats=True)
+
+    fv_all, st_all = step()
     torch.cuda.synchronize(dev)
-    parity = None
-    if rank == 0 and world == 1 and args.cpu_seconds > 0:  # cpu_baseline leg (the only place the oracle
-        # runs here): a 20k-row sample through the same entry points, checked before timing
-        import oracle
-        m = min(n, 20000)
-        s1 = fv.stats_batched(Xd[:m].contiguous(), torch.tensor([0, m], dtype=torch.int64, device=dev), gmm)
-        got = fv.finalize(s1, gmm).cpu().numpy()[0]
-        ref = oracle.encode(X[:m], *gmm_np)
-        err = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
-        parity = {"sample_rows": m, "max_rel_l2": err, "tolerance": 1e-4}
-        if err > 1e-4:
-            raise SystemExit(f"parity failure before timing: {err}")
+    # self-check on every rank, no oracle: the all-reduced statistics satisfy sum_j S0_j = N (every
+    # posterior row sums to 1, Alg.1 l.6-14), the FV is finite and unit-norm, no range flag; and when
+    # the set is BASELINE's full C5, its FV and S0 against the oracle-written golden (same global set)
+    sc = st_all.cpu().numpy()[0]
+    n_all = nfr * frame
+    check = {"N": float(sc[0]), "sumS0_rel_err": abs(float(sc[1:1 + K5].sum()) - n_all) / n_all}
+    if sc[0] != n_all or check["sumS0_rel_err"] > 1e-5:
+        raise SystemExit(f"C5 self-check failed before timing: {check}")
+    self_check_fvs(fv_all.reshape(1, -1), "C5")
+    if int(fv.range_flags(ws, n, 1, gmm).max().item()) != 0:
+        raise SystemExit("C5: range flag set before timing")
+    gpath = os.path.join(ROOT, "tests", "golden", "large_c5.npz")
+    if os.path.exists(gpath) and n_all == 10_000_000:
+        g = np.load(gpath)
+        if "fv" in g:
+            got = fv_all.cpu().numpy().astype(np.float64)
+            check["fv_rel_l2_vs_oracle_golden"] = float(np.linalg.norm(got - g["fv"]) / np.linalg.norm(g["fv"]))
+            check["S0_max_rel_err_vs_oracle_golden"] = float(np.max(np.abs(sc[1:1 + K5] - g["stats"][1:1 + K5])
+                                                                  / g["stats"][1:1 + K5]))
+            if check["fv_rel_l2_vs_oracle_golden"] > 1e-4:
+                raise SystemExit(f"C5 full-set parity failure before timing: {check}")
+    parity = {"self_check": check, "tolerance": {"fv_rel_l2": 1e-4, "sumS0_rel": 1e-5}}
     clk = ClockSampler(local, pci_bus_id(dev)).__enter__()
     for _ in range(max(3, args.warmup)):
         step()
@@ -332,7 +505,6 @@ def run_c5(args, rank, world, local):
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    n_all = (args.c5_n // frame) * frame
     value = n_all * args.steps / (total_ms * 1e-3)
 
     # end to end: pinned host shard -> device, statistics, all-reduce, finalize, FV -> host (host clock)
@@ -366,7 +538,7 @@ def run_c5(args, rank, world, local):
             torch.distributed.destroy_process_group()
         return
     flop = 4 * K5 * (2 * D5 + 1)
-    peak_tf, peak_src = tensor_peak()
+    peak_tf, other_tf, peak_src = peak_for(total_ms * 1e-3)
     achieved = flop * n / (kms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -379,7 +551,8 @@ def run_c5(args, rank, world, local):
                    "parallelism": f"descriptor-sharded x{world}, all_reduce(SUM) of [N,S0,S1,S2]",
                    "l2": f"inputs {n * D5 * 4 / 1e9:.2f} GB per rank > 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tf, "traffic": None, "kernel": "k_stats_w", "kernel_ms": kms,
+                     "frac": achieved / peak_tf, "frac_other_peak": achieved / other_tf, "traffic": None,
+                     "kernel": "k_stats_w", "kernel_ms": kms,
                      "kernel_share_of_step": kms / (total_ms / args.steps), "flop_per_desc": flop,
                      "peak_source": peak_src},
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches[0] * args.steps, "parity": parity,
@@ -406,7 +579,9 @@ def run_em(args, rank, world, local):
     from paper_1604_03498_b200 import dist as fvdist
     n_frames = 256 * 4  # 1024 blocks of 5000 = 5.12 M rows
     true_np = fvgen.make_gmm(K, D, seed=1604)
-    X = fvgen.make_frames(true_np, n_frames, PER_FRAME, seed=1604 + 30000 + rank * 1_000_003).reshape(-1, D)
+    # rank r: frames [r n_frames, (r+1) n_frames) of one global pool (rank 0's = tests/golden/large_pool64.npz)
+    X = fvgen.make_frames(true_np, n_frames, PER_FRAME, seed=1604 + 30000, start=rank * n_frames,
+                          total=world * n_frames).reshape(-1, D)
     n = X.shape[0]
     init_np = fvgen.make_gmm(K, D, seed=1704)
     Xd = torch.from_numpy(X).to(dev)
@@ -425,12 +600,27 @@ def run_em(args, rank, world, local):
             new, ll = fvdist.em_step_sharded(Xd, g_a, estep_fn=lambda Xs: fv.gmm_estep(Xs, g_a, ws=ws),
                                              mstep_fn=lambda st: fv.gmm_mstep(st, g_a, ws=ws))
             lls.append(ll)
-        else:
-            fv.gmm_em_step(Xd, g_a, ws=ws, out=g_a)
+            return new
+        fv.gmm_em_step(Xd, g_a, ws=ws, out=g_a)
+        return g_a
 
-    step()
+    new = step()
     torch.cuda.synchronize(dev)
-    parity = None
+    # self-check on every rank (no oracle): the new priors sum to 1 and the model is finite; at N = 1 the
+    # step against the oracle-written golden EM step of the same pool (tests/golden/large_pool64.npz)
+    pis, mus, vs = (t.double().cpu().numpy() for t in (new.weights, new.means, new.sigmas))
+    em_check = {"sum_pi_err": abs(float(pis.sum()) - 1.0)}
+    if not (np.isfinite(mus).all() and np.isfinite(vs).all() and (vs > 0).all()) or em_check["sum_pi_err"] > 1e-6:
+        raise SystemExit(f"EM self-check failed before timing: {em_check}")
+    gpath = os.path.join(ROOT, "tests", "golden", "large_pool64.npz")
+    if world == 1 and os.path.exists(gpath):
+        g = np.load(gpath)
+        em_check["mu_err_over_sd_vs_oracle_golden"] = float(np.max(np.abs(mus - g["em_mu"]) / np.sqrt(g["em_var"])))
+        em_check["var_rel_err_vs_oracle_golden"] = float(np.max(np.abs(vs - g["em_var"]) / g["em_var"]))
+        em_check["pi_abs_err_vs_oracle_golden"] = float(np.max(np.abs(pis - g["em_pi"])))
+        if em_check["mu_err_over_sd_vs_oracle_golden"] > 1e-4:
+            raise SystemExit(f"EM full-pool parity failure before timing: {em_check}")
+    parity = {"self_check": em_check}
     if rank == 0 and world == 1 and args.cpu_seconds > 0:  # cpu_baseline leg: a 20k-row sample through
         # the same entry point vs the oracle's EM step, checked before timing
         import oracle
@@ -439,8 +629,8 @@ def run_em(args, rank, world, local):
         pi_r, mu_r, var_r, ll_r = oracle.em_step(X[:m], *init_np)
         err_mu = float(np.max(np.abs(new.means.cpu().numpy() - mu_r) / np.sqrt(var_r)))
         err_ll = abs(float(ll.item()) - ll_r) / m
-        parity = {"sample_rows": m, "max_mu_err_over_sd": err_mu, "loglik_err_per_desc": err_ll,
-                  "tolerance": {"mu_over_sd": 1e-3, "loglik_per_desc": 2e-5}}
+        parity.update({"sample_rows": m, "max_mu_err_over_sd": err_mu, "loglik_err_per_desc": err_ll,
+                       "tolerance": {"mu_over_sd": 1e-3, "loglik_per_desc": 2e-5}})
         if err_ll > 2e-5:
             raise SystemExit(f"EM parity failure before timing: {parity}")
     clk = ClockSampler(local, pci_bus_id(dev)).__enter__()
@@ -479,7 +669,7 @@ def run_em(args, rank, world, local):
         if world > 1:
             torch.distributed.destroy_process_group()
         return
-    peak_tf, peak_src = tensor_peak()
+    peak_tf, other_tf, peak_src = peak_for(total_ms * 1e-3)
     achieved = FLOP_PER_DESC * n / (ms * 1e-3) / 1e12
     line = {
         "metric": f"descriptors/sec per GMM EM iteration (K={K},D={D})", "value": world * n / (ms * 1e-3),
@@ -489,7 +679,8 @@ def run_em(args, rank, world, local):
                                "posteriors, from a seeded init", "parallelism": f"descriptor-sharded x{world}"
                                + (", all_reduce of stats + loglik" if world > 1 else "")},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tf, "traffic": None, "kernel": "k_stats (whole EM step timed)",
+                     "frac": achieved / peak_tf, "frac_other_peak": achieved / other_tf, "traffic": None,
+                     "kernel": "k_stats (whole EM step timed)",
                      "flop_per_desc": FLOP_PER_DESC, "peak_source": peak_src},
         "clocks": clk.summary(), "gpu_launches": None, "parity": parity, "cpu_baseline": cpu, "e2e": None,
     }
@@ -603,7 +794,11 @@ def run_embed(args, rank, world, local):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -623,25 +818,35 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     import paper_1604_03498_b200 as fv
+    from paper_1604_03498_b200 import dist as fvdist
 
-    frames = args.frames
-    gmm_np, X, offsets = make_stream(frames, rank)
+    gmm_np, X, offsets_global, _ = make_stream(args.frames, rank, world)
+    shard = fvdist.FrameShard(offsets_global, rank, world, device=dev)  # this rank's frames, plan built once
+    frames = shard.hi - shard.lo
+    offsets = offsets_global[shard.lo:shard.hi + 1] - offsets_global[shard.lo]
     n_total = X.shape[0]
     gmm = fv.GMM(*gmm_np, device=dev)
     Xd = torch.from_numpy(X).to(dev)
-    offd = torch.from_numpy(offsets).to(dev)
+    offd = shard.local_offsets
     ws = fv.Workspace(device=dev)
     ws.ensure(fv.workspace_bytes(n_total, frames, K, D))
     fv.gmm_prepare(gmm, ws)
     out = torch.empty(frames, 2 * K * D, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        fv.encode_batched(Xd, offd, gmm, threshold=TAU, ws=ws, prepared=True, out=out)
+    def enc(Xs, offs):
+        return fv.encode_batched(Xs, offs, gmm, threshold=TAU, ws=ws, prepared=True, out=out)
 
-    # correctness before timing: sampled frames against the oracle
+    def step():  # frame sharding through dist.encode_frames_sharded (no collective on the data path)
+        fvdist.encode_frames_sharded(Xd, None, gmm, shard=shard, rows_local=True, encode_fn=enc)
+
+    # correctness before timing: every rank self-checks (finite, unit norm, no range flag);
+    # at N = 1 the cpu_baseline leg also checks sampled frames against the oracle
     step()
     torch.cuda.synchronize(dev)
+    self_check_fvs(out, "C4")
+    if int(fv.range_flags(ws, n_total, frames, gmm).max().item()) != 0:
+        raise SystemExit("C4: range flag set before timing")
     parity = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:  # cpu_baseline leg: sampled outputs vs the oracle
         import oracle
@@ -822,16 +1027,22 @@ def main():
             lambda: fv.encode(x_pg, gmm, threshold=TAU, ws=ws_pg, prepared=True, out=o1))
         latency["paper_geometry_workload"] = f"one frame, {n_pg} descriptors (paper geometry), K={K}, D={D}, tau={TAU}"
 
+    legs = None
+    if not args.no_legs:
+        legs = run_legs(fv, gmm, gmm_np, dev, stream, rank, world)
+
     cpu = None
+    stress = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         cpu = cpu_baseline_run(gmm_np, X, frames, args.cpu_seconds)
+        stress = stress_errors(fv, dev)
 
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
         return
 
-    peak_tf, peak_src = tensor_peak()
+    peak_tf, other_tf, peak_src = peak_for(total_ms * 1e-3)
     kms = statistics.mean(kstats_ms)
     achieved = FLOP_PER_DESC * n_total / (kms * 1e-3) / 1e12
     traffic = None
@@ -854,7 +1065,8 @@ def main():
                    "parallelism": f"frame-sharded x{world}, no collective",
                    "l2": f"inputs {n_total * D * 4 / 1e9:.2f} GB per rank > 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "tensor", "achieved": achieved,
-                     "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
+                     "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf,
+                     "frac_other_peak": achieved / other_tf, "traffic": traffic,
                      "kernel": "k_stats", "kernel_ms": kms, "kernel_share_of_step": kms / ms_per_step,
                      "flop_per_desc": FLOP_PER_DESC,
                      "issued_tensor_frac": achieved * ISSUED_FLOP_PER_DESC / FLOP_PER_DESC / peak_tf,
@@ -864,6 +1076,8 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "parity": parity,
         "frame_latency": latency,
+        "legs": legs,
+        "stress": stress,
         "monitoring": monitoring,
         "cpu_baseline": cpu,
         "context": {"paper": "34 ms per 320x240 frame and ~12x over 1-thread CPU, end-to-end incl. dense SIFT, "

@@ -60,33 +60,49 @@ def make_descriptors(gmm, N: int, seed: int, bg_frac: float = 0.05) -> np.ndarra
     return x.astype(np.float32)
 
 
-def make_frames(gmm, frames: int, per_frame: int, seed: int, block: int = 64, bg_frac: float = 0.05) -> np.ndarray:
+def make_frames(gmm, frames: int, per_frame: int, seed: int, block: int = 64, bg_frac: float = 0.05,
+                start: int = 0, total: int | None = None) -> np.ndarray:
     """Large streams (bench): frames x per_frame descriptors from the same recipe, drawn in float32
-    blocks of `block` frames (one seeded generator per block).  Background rows are placed at random
-    positions (each row with probability bg_frac) instead of first-then-shuffle; same distribution."""
+    blocks of `block` frames (one seeded generator per block, seeded by the block's first frame).
+    Background rows are placed at random positions (each row with probability bg_frac) instead of
+    first-then-shuffle; same distribution.
+
+    `start` / `total` select frames [start, start + frames) of a stream of `total` frames (default
+    start + frames): the rows are exactly those of make_frames(gmm, total, ...)[start*pf:(start+frames)*pf],
+    so the ranks of a sharded run draw disjoint slices of one fixed set whatever the world size."""
     pi, mu, var = gmm
     K, D = mu.shape
+    total = start + frames if total is None else int(total)
+    assert 0 <= start and start + frames <= total
     cdf = np.cumsum(pi.astype(np.float64))
     cdf /= cdf[-1]
     sd = np.sqrt(var.astype(np.float64)).astype(np.float32)
     s = spread(D).astype(np.float32)
     X = np.empty((frames * per_frame, D), dtype=np.float32)
 
-    def fill(f0):  # independent per block: same result for any thread count
-        rng = np.random.default_rng(seed + f0)
-        n = min(block, frames - f0) * per_frame
+    def fill(g0):  # independent per block: same result for any thread count or slice
+        rng = np.random.default_rng(seed + g0)
+        nf = min(block, total - g0)
+        n = nf * per_frame
         c = np.minimum(np.searchsorted(cdf, rng.random(n)), K - 1)
         z = rng.standard_normal((n, D), dtype=np.float32)
         bg = rng.random(n) < bg_frac
-        xb = X[f0 * per_frame:f0 * per_frame + n]
+        a, b = max(g0, start), min(g0 + nf, start + frames)  # overlap with the requested frames
+        whole = a == g0 and b == g0 + nf
+        xb = X[(a - start) * per_frame:(b - start) * per_frame] if whole else np.empty((n, D), np.float32)
         np.multiply(sd[c], z, out=xb)
         xb += mu[c]
         xb[bg] = s * z[bg]
+        if not whole:
+            X[(a - start) * per_frame:(b - start) * per_frame] = xb[(a - g0) * per_frame:(b - g0) * per_frame]
 
     from concurrent.futures import ThreadPoolExecutor
     import os
+    if frames == 0:
+        return X
+    first = (start // block) * block
     with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
-        list(ex.map(fill, range(0, frames, block)))
+        list(ex.map(fill, range(first, start + frames, block)))
     return X
 
 

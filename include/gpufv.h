@@ -23,11 +23,12 @@
  *     reductions): identical inputs give bitwise-identical outputs.
  *   - Limits: 1 <= K <= 512, 1 <= D <= 128, D % 4 == 0 (caller pads, reading A13), X 16-byte aligned.
  *     D <= 64 runs the narrow kernel (128 Gaussians per CTA); 64 < D <= 128 the wide one (64 per CTA).
- *   - Device data is not validated (that would need a kernel + sync): var <= 0, pi <= 0 or non-finite
- *     X propagate NaN into that image's output only.  Descriptors with |x-c|/rms >= 255 in some
- *     dimension (c, rms: GMM-weighted mean/RMS) overflow the fp16 split operands, and
- *     so does a component whose standard deviation in some dimension is below ~rms/150 (its
- *     -1/(2 var) coefficient exceeds the fp16 range); both give NaN/inf for the affected images.
+ *   - Device data is not validated synchronously (that would need a kernel + sync): pi <= 0 gives NaN
+ *     for the images it touches.  Inputs outside the fp16 operand range of the split contractions —
+ *     descriptors with |x-c|/rms >= ~256 in some dimension (c, rms: GMM-weighted mean/RMS), components
+ *     with a standard deviation below ~rms/150 in some dimension, var <= 0, non-finite X — make the
+ *     affected images' outputs NaN (never finite garbage) and are reported per image by
+ *     fv_range_flags().
  *   - Synchronous argument errors return a status; asynchronous CUDA errors are reported by the
  *     next call or by cudaGetLastError.  fv_last_error() returns a thread-local detail string.
  *   - Thread safety: reentrant; concurrent calls need distinct workspaces.
@@ -91,8 +92,11 @@ fv_status fv_encode_batched(const float *X, const int64_t *offsets, int batch, i
 /* Same as fv_encode_batched but X_host / offsets_host / out_host are HOST buffers (pinned for full
  * PCIe speed); the GMM arrays stay device pointers (a resident model).  The batch is processed in up to
  * 16 image chunks: the host->device copy of chunk k+1 and the device->host copy of chunk k-1 run on two
- * internal streams (created and destroyed by the call) while chunk k is encoded on `stream`; the call
- * synchronises all three before returning.  Each chunk runs the device path on its own images, so
+ * internal streams while chunk k is encoded on `stream`; the internal streams first wait for all work
+ * already queued on `stream`, and the call synchronises all three before returning.  The two streams
+ * and their events are created on the first host call of a (thread, device) and reused afterwards.
+ * offsets_host is validated before any copy (offsets[0] == 0, non-decreasing, offsets[batch] ==
+ * n_total; else FV_ERR_ARG).  Each chunk runs the device path on its own images, so
  * results equal fv_encode_batched's to rounding (same images, different static schedule) and are
  * bitwise repeatable across calls.  ws >= fv_workspace_bytes_host(...). */
 fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total,
@@ -205,6 +209,19 @@ fv_status fv_embed_encode_batched(const float *raw, const float *xy, const int64
 fv_status fv_posteriors(const float *X, int64_t N, int D, const float *weights, const float *means,
                         const float *sigmas, int K, float threshold, unsigned flags, float *gamma,
                         void *ws, size_t ws_bytes, fv_stream_t stream);
+
+/* Range report.  The contractions run on fp16 hi/lo split operands, so a descriptor with
+ * |x_k - c_k| >= ~256 RMS_k in some dimension (c, RMS: the GMM-weighted mean and RMS of dimension k),
+ * a component whose standard deviation in some dimension is below ~RMS_k/150, or non-finite input,
+ * cannot be represented.  Such inputs are never turned into finite garbage: every row whose
+ * log-likelihoods are not all finite gets NaN posteriors, so its image's statistics / FV / scores are
+ * NaN, and the image is flagged.  After an fv_encode*, fv_stats_batched, fv_posteriors or E-step call
+ * made with `ws`, this writes (stream-ordered, device int32 array of `batch` entries)
+ *   flags_out[b] = bit 0: image b had a row with non-finite log-likelihoods;
+ *                  bit 1: the prepared GMM has a coefficient outside the fp16 range (all images NaN).
+ * n_total, batch, K, D are those of that call (they locate the flags in ws); 0 everywhere = in range. */
+fv_status fv_range_flags(const void *ws, size_t ws_bytes, int64_t n_total, int batch, int K, int D,
+                         int32_t *flags_out, fv_stream_t stream);
 
 /* Profiling hook (bench accounting): when set, every k_stats launch made by this thread is bracketed
  * by cudaEventRecord(start/stop, stream) so the caller can time the dominant kernel alone with CUDA

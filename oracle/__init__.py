@@ -18,6 +18,7 @@ from .oracle import (  # noqa: F401
     build,
     embed,
     em_step,
+    em_step_blocked,
     encode,
     encode_batched,
     fv_from_stats,
@@ -28,4 +29,5 @@ from .oracle import (  # noqa: F401
     score,
     stats,
     stats_batched,
+    stats_blocked,
 )

@@ -261,3 +261,82 @@ def embed(raw, xy, offsets, wh, pca_mean, pca_basis) -> np.ndarray:
     img = np.repeat(np.arange(len(off) - 1), np.diff(off))
     proj = (raw - mean[None, :]) @ B.T
     return np.concatenate([proj, xy / wh[img]], axis=1)
+
+
+# ------------------------------------------------------------------ large single sets (C5, EM pool)
+# Compositions for sets too large to convert to float64 in one piece.  They add no arithmetic: the
+# statistics are sums over descriptors (reading A19), computed block by block with the same C code
+# (fixed blocks of `block` rows, the paper's "one copy ... for each block" reduction, Alg.3)
+# and summed in block order, so the result does not depend on the thread count.
+
+def _block_ranges(N: int, block: int):
+    return [(a, min(a + block, N)) for a in range(0, N, block)]
+
+
+def stats_blocked(X, priors, means, variances, threshold: float = 0.0, block: int = 50_000,
+                  nthreads: int = 0) -> np.ndarray:
+    """stats() of one large set (any size, float32 X): [N, S0, S1, S2] about c, summed over fixed row
+    blocks in order.  Equal to stats() up to fp64 summation order (tests/test_oracle.py)."""
+    w, m, v, K, D = _gmm(priors, means, variances)
+    N = X.shape[0]
+    chunk = block * max(1, max_threads() if nthreads <= 0 else nthreads)
+    total = np.zeros(1 + K * (2 * D + 1))
+    for c0 in range(0, N, chunk):
+        c1 = min(c0 + chunk, N)
+        off = np.array([a for a, _ in _block_ranges(c1 - c0, block)] + [c1 - c0], dtype=np.int64)
+        part = stats_batched(X[c0:c1], off, w, m, v, threshold=threshold, nthreads=nthreads)
+        for row in part:  # block order
+            total += row
+    return total
+
+
+def em_step_blocked(X, priors, means, variances, var_floor_abs: float = 1e-6, var_floor_rel: float = 1e-4,
+                    prior_floor: float = 1e-8, block: int = 50_000, workers: int = 0):
+    """em_step() for a large float32 set, in two passes over fixed row blocks (same definitions, each
+    block's partial sums added in block order):
+      pass 1: N_j = sum gamma_ij, sum_i gamma_ij x_i, sum_i x_i, LL = sum_i ln p(x_i)
+      pass 2: sum_i gamma_ij (x_ik - mu_jk)^2 and sum_i (x_ik - mean_k)^2 about the pass-1 means.
+    Posteriors come from the C oracle (fvo_posteriors) per block; blocks run on a thread pool (the C
+    call and numpy release the GIL) and are combined in block order."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    w, m, v, K, D = _gmm(priors, means, variances)
+    N = X.shape[0]
+    ranges = _block_ranges(N, block)
+    workers = workers or max_threads()
+
+    def p1(r):
+        Xb = _d(X[r[0]:r[1]])
+        g = posteriors(Xb, w, m, v)
+        return g.sum(0), g.T @ Xb, Xb.sum(0), float(loglik_rows(Xb, w, m, v).sum())
+
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        parts = list(ex.map(p1, ranges))
+    Nj = np.zeros(K); Sx = np.zeros((K, D)); xs = np.zeros(D); LL = 0.0
+    for a, b, c, d in parts:
+        Nj += a; Sx += b; xs += c; LL += d
+    mu = m.copy()
+    nz = Nj > 0
+    mu[nz] = Sx[nz] / Nj[nz, None]
+    gmean = xs / N
+
+    def p2(r):
+        Xb = _d(X[r[0]:r[1]])
+        g = posteriors(Xb, w, m, v)
+        sv = np.empty((K, D))
+        for j in range(K):
+            sv[j] = (g[:, j:j + 1] * (Xb - mu[j]) ** 2).sum(axis=0)
+        return sv, ((Xb - gmean) ** 2).sum(axis=0)
+
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        parts = list(ex.map(p2, ranges))
+    Sv = np.zeros((K, D)); gv = np.zeros(D)
+    for a, b in parts:
+        Sv += a; gv += b
+    var = v.copy()
+    var[nz] = Sv[nz] / Nj[nz, None]
+    floor = np.maximum(var_floor_abs, var_floor_rel * gv / N)
+    var = np.maximum(var, floor[None, :])
+    pi = np.maximum(Nj / N, prior_floor)
+    pi = pi / pi.sum()
+    return pi, mu, var, LL

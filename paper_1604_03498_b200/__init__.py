@@ -17,7 +17,7 @@ __all__ = [
     "GMM", "Workspace", "lib", "lib_path", "workspace_bytes", "gmm_prepare", "encode", "encode_batched",
     "encode_batched_host", "stats_batched", "finalize", "posteriors", "last_launch_count", "profile_events",
     "encode_scored_batched", "encode_scored_batched_host", "MAX_CLASSES", "gmm_estep", "gmm_mstep", "gmm_em_step",
-    "gmm_fit", "embed", "embed_encode_batched", "FVError",
+    "gmm_fit", "embed", "embed_encode_batched", "FVError", "range_flags",
 ]
 
 NORM_IMPROVED = 0
@@ -82,6 +82,8 @@ lib.fv_last_error.restype = _c.c_char_p
 lib.fv_last_launch_count.argtypes = []
 lib.fv_last_launch_count.restype = _i32
 lib.fv_version.restype = _i32
+lib.fv_range_flags.argtypes = [_vp, _sz, _i64, _i32, _i32, _i32, _vp, _vp]
+lib.fv_range_flags.restype = _i32
 lib.fv_profile_events.argtypes = [_vp, _vp]
 lib.fv_profile_events.restype = None
 
@@ -189,6 +191,16 @@ def _check_X(X, D):
         raise ValueError(f"X must be a contiguous float32 CUDA tensor of shape (N, {D})")
 
 
+def _check_offsets(offsets, X=None):
+    """offsets: contiguous int64 CUDA tensor (batch + 1,) on X's device (a host tensor would be handed to
+    the kernels as a device pointer)."""
+    if not (offsets.is_cuda and offsets.dtype == torch.int64 and offsets.is_contiguous() and offsets.dim() == 1
+            and offsets.shape[0] >= 1):
+        raise ValueError("offsets must be a contiguous 1-D int64 CUDA tensor of batch + 1 entries")
+    if X is not None and offsets.device != X.device:
+        raise ValueError("offsets and X must be on the same device")
+
+
 def encode(X, gmm: GMM, threshold: float = 0.0, mode: int = NORM_IMPROVED, ws: Workspace | None = None,
            prepared: bool = False, out=None):
     """One descriptor set (N x D) -> FV (2KD,)."""
@@ -207,8 +219,7 @@ def encode_batched(X, offsets, gmm: GMM, threshold: float = 0.0, mode: int = NOR
                    ws: Workspace | None = None, prepared: bool = False, out=None):
     """Independent images: X (n_total x D), offsets (batch+1, int64 CUDA) -> (batch, 2KD)."""
     _check_X(X, gmm.D)
-    if not (offsets.is_cuda and offsets.dtype == torch.int64 and offsets.is_contiguous()):
-        raise ValueError("offsets must be a contiguous int64 CUDA tensor")
+    _check_offsets(offsets, X)
     B = offsets.shape[0] - 1
     ws, grown = _ws(ws, workspace_bytes(X.shape[0], B, gmm.K, gmm.D), X.device)
     prepared = prepared and not grown
@@ -244,6 +255,7 @@ def stats_batched(X, offsets, gmm: GMM, threshold: float = 0.0, ws: Workspace | 
     """Sufficient statistics (batch, 1 + K(2D+1)) float64 about c (reading A19); they add across
     disjoint descriptor shards."""
     _check_X(X, gmm.D)
+    _check_offsets(offsets, X)
     B = offsets.shape[0] - 1
     ws, grown = _ws(ws, workspace_bytes(X.shape[0], B, gmm.K, gmm.D), X.device)
     prepared = prepared and not grown
@@ -284,6 +296,16 @@ def posteriors(X, gmm: GMM, threshold: float = 0.0, raw_loglik: bool = False, ws
     return g
 
 
+def range_flags(ws: Workspace, n_total: int, batch: int, gmm: GMM):
+    """Per-image range report (int32, batch) of the last encode / stats / posteriors / E-step call made with
+    ``ws`` on (n_total descriptors, batch images, gmm): bit 0 = the image had a row with non-finite
+    log-likelihoods (a descriptor outside the fp16 operand range or non-finite input), bit 1 = the GMM has
+    a coefficient outside the fp16 range.  Flagged images' outputs are NaN (include/gpufv.h)."""
+    flags = torch.empty(max(int(batch), 0), dtype=torch.int32, device=ws.device)
+    _check(lib.fv_range_flags(*ws.args(), int(n_total), int(batch), gmm.K, gmm.D, _ptr(flags), _stream()))
+    return flags
+
+
 def _classifier(svm_w, svm_b, gmm: GMM):
     dim = 2 * gmm.K * gmm.D
     if not (svm_w.is_cuda and svm_w.dtype == torch.float32 and svm_w.is_contiguous()):
@@ -301,6 +323,7 @@ def encode_scored_batched(X, offsets, gmm: GMM, svm_w, svm_b=None, threshold: fl
     the finalize kernel.  With return_fv (or an ``out`` tensor) the FVs are also written and returned
     as (scores, fv); otherwise they never reach HBM."""
     _check_X(X, gmm.D)
+    _check_offsets(offsets, X)
     W, n_cls = _classifier(svm_w, svm_b, gmm)
     B = offsets.shape[0] - 1
     need = int(lib.fv_workspace_bytes_scored(X.shape[0], B, gmm.K, gmm.D, n_cls, 0, 0))
@@ -412,11 +435,12 @@ def _check_embed_inputs(raw, xy, offsets, img_wh, pca_mean, pca_basis):
     for name, t, cols in (("raw", raw, 128), ("xy", xy, 2), ("img_wh", img_wh, 2)):
         if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.dim() == 2 and t.shape[1] == cols):
             raise ValueError(f"{name} must be a contiguous float32 CUDA tensor (*, {cols})")
-    if not (offsets.is_cuda and offsets.dtype == torch.int64):
-        raise ValueError("offsets must be an int64 CUDA tensor")
-    if not (pca_basis.is_cuda and pca_basis.dtype == torch.float32 and pca_basis.is_contiguous()
-            and pca_basis.shape[1] == 128 and pca_mean.numel() == 128):
-        raise ValueError("pca_mean (128,) and pca_basis (m, 128) must be contiguous float32 CUDA tensors")
+    _check_offsets(offsets, raw)
+    for name, t in (("pca_mean", pca_mean), ("pca_basis", pca_basis)):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.device == raw.device):
+            raise ValueError(f"{name} must be a contiguous float32 CUDA tensor on raw's device")
+    if not (pca_basis.dim() == 2 and pca_basis.shape[1] == 128 and pca_mean.numel() == 128):
+        raise ValueError("pca_mean must have 128 entries and pca_basis shape (m, 128)")
     return pca_basis.shape[0]
 
 

@@ -122,7 +122,8 @@ struct Layout {
   int C, Kp, ncl, dpad;  // cluster size, padded K, clusters, padded D (64 | 128)
   int64_t n_total, nslots;                                         // segment slots (cluster, image)
   size_t wimg, bias, xshift, xscale, cshift, bscratch, bmax, pscale, xinv, coef;  // prepared GMM (head of ws)
-  size_t tiles, off1, cstart, cown, norm2, s0slots, slots;  // per call
+  size_t gflag;                                           // GMM range flag (prepared head, after bmax)
+  size_t tiles, off1, cstart, cown, norm2, rflags, s0slots, slots;  // per call
   size_t spart;                                           // fused scoring partial dots (n_cls > 0)
   size_t llrows, llparts, emstats;                        // EM: per-row log2-likelihoods, reduction, stats
   size_t emb;                                             // embedded descriptors (n_total x ldx), NEXT-2
@@ -159,7 +160,8 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.xscale = o;   o = align_up(o + kDMax * 4, 256);
   L.cshift = o;   o = align_up(o + kDMax * 8, 256);
   L.bscratch = o; o = align_up(o + (size_t)L.Kp * 8, 256);
-  L.bmax = o;     o = align_up(o + 8, 256);
+  L.bmax = o;     o = align_up(o + 16, 256);
+  L.gflag = L.bmax + 8;
   L.pscale = o;   o = align_up(o + (size_t)2 * L.Kp * 8, 256);
   L.xinv = o;     o = align_up(o + kDMax * 8, 1024);
   L.coef = o;     o = align_up(o + (size_t)3 * kDMax * L.Kp * 8, 1024);
@@ -168,6 +170,7 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.cstart = o;   o = align_up(o + (size_t)(L.ncl + 1) * 4, 256);
   L.cown = o;     o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 8, 256);
   L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * (kFinMaxParts * 8 + 4), 1024);  // norm parts + tickets
+  L.rflags = o;   o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 4, 256);
   L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * 4 * L.Kp * 4, 1024);
   L.slots = o;    o = align_up(o + (size_t)L.nslots * 2 * L.dpad * L.Kp * 4, 1024);
   L.spart = o;    o = align_up(o + (size_t)(n_cls > 0 ? batch : 0) * kFinMaxParts * n_cls * 8, 1024);
@@ -229,12 +232,13 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
                       void *ws, cudaStream_t st) {
   const int sd = (flags & FV_SIGMA_IS_STDDEV) ? 1 : 0;
   k_prep_shift<<<1, kPrepThreads, 0, st>>>(w, mu, sg, K, D, L.Kp, sd, (double *)at(ws, L.cshift), (float *)at(ws, L.xshift),
-                                  (float *)at(ws, L.xscale), (double *)at(ws, L.pscale), (double *)at(ws, L.xinv));
+                                  (float *)at(ws, L.xscale), (double *)at(ws, L.pscale), (double *)at(ws, L.xinv),
+                                  (int *)at(ws, L.gflag));
   k_prep_bias<<<K, kDMax, 0, st>>>(w, mu, sg, D, sd, (const double *)at(ws, L.cshift), (double *)at(ws, L.bscratch));
   k_prep_bias_final<<<1, 512, 0, st>>>(K, L.Kp, (const double *)at(ws, L.bscratch), (float *)at(ws, L.bias),
                                        (double *)at(ws, L.bmax));
   k_prep_w<<<L.Kp, 2 * L.dpad, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
-                                 at(ws, L.wimg), (double *)at(ws, L.coef), is_wide(K, D) ? 1 : 0);
+                                 at(ws, L.wimg), (double *)at(ws, L.coef), is_wide(K, D) ? 1 : 0, (int *)at(ws, L.gflag));
   g_launches += 4;
   return cuda_check("k_prep");
 }
@@ -242,13 +246,14 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
 // a2-a6 over a batch: schedule + persistent stats kernel.  gamma (optional) for fv_posteriors.
 fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets, int64_t n_single, int batch, int D,
                        int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st,
-                       float *loglik_rows = nullptr, int ldx = 0) {
+                       float *loglik_rows = nullptr, int ldx = 0, int rf_base = 0) {
   if (ldx <= 0) ldx = D;
+  int *rflags = (int *)at(ws, L.rflags) + rf_base;
   // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
   int64_t *off1 = (int64_t *)at(ws, L.off1);
   unsigned *counters = (unsigned *)((double *)at(ws, L.norm2) + (size_t)(batch > 0 ? batch : 1) * kFinMaxParts);
   k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles), L.ncl,
-                                 (int *)at(ws, L.cstart), (int *)at(ws, L.cown), counters);
+                                 (int *)at(ws, L.cstart), (int *)at(ws, L.cown), counters, rflags);
   if (!offsets) offsets = off1;
   g_launches += 1;
   Stats2Params p;
@@ -264,6 +269,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.gamma_out = gamma;
   p.loglik_out = loglik_rows;
   p.trace = g_trace;
+  p.rflags = rflags;
   p.batch = batch;
   p.D = D;
   p.K = K;
@@ -287,7 +293,10 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
     cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
     cuuint32_t box[2] = {32, 128};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(X), dims, strides, box, estr,
+    // an empty launch (n_total == 0, X typically NULL) loads no tile, but the map still needs a valid
+    // global address: point it at the workspace
+    float *xmap = (X && L.n_total > 0) ? const_cast<float *>(X) : reinterpret_cast<float *>(ws);
+    CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, xmap, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(FV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -452,7 +461,7 @@ struct Scoring {
 fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D,
                               const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
                               float *out, void *ws, size_t ws_bytes, cudaStream_t st, const Layout *Lin,
-                              const Scoring &sc = Scoring(), int ldx = 0) {
+                              const Scoring &sc = Scoring(), int ldx = 0, int rf_base = 0) {
   Layout L;
   if (Lin) L = *Lin;
   else if (!make_layout(n_total, batch, K, D, false, L, sc.n_cls)) return fail(FV_ERR_CUDA, "occupancy query failed");
@@ -460,7 +469,8 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   if (!(flags & FV_PREPARED))
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
   if (batch == 0) return FV_OK;
-  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx)) return s;
+  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx, rf_base))
+    return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   f.out = out;
   f.svm_w = sc.w; f.svm_b = sc.b; f.n_cls = sc.n_cls; f.scores = sc.scores;
@@ -543,14 +553,47 @@ fv_status fv_encode(const float *X, int64_t N, int D, const float *w, const floa
 
 namespace {
 
+// Internal streams / events of the host pipeline: created once per (thread, device) on first use and
+// reused by every later call (never destroyed: they live as long as the thread's CUDA context), so a
+// call makes no stream or event allocations after the first.
+constexpr int kHostChunks = 16;
+struct HostPipe {
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t ev[2 * kHostChunks + 1] = {};
+  bool ok = false;
+};
+fv_status host_pipe(HostPipe *&hp) {
+  thread_local HostPipe pipes[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cuda_check("cudaGetDevice");
+  hp = &pipes[dev];
+  if (hp->ok) return FV_OK;
+  if (cudaStreamCreateWithFlags(&hp->cin, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&hp->cout, cudaStreamNonBlocking) != cudaSuccess)
+    return cuda_check("stream create");
+  for (auto &e : hp->ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return cuda_check("event create");
+  hp->ok = true;
+  return FV_OK;
+}
+
 // Host-buffer pipeline shared by fv_encode_batched_host and fv_encode_scored_batched_host: the result
 // per image is the FV (2KD floats) or, with scoring, its n_cls scores.
 fv_status encode_host_impl(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total, int D,
                            const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
                            float *res_host, const Scoring &sc_in, void *ws, size_t ws_bytes, cudaStream_t st) {
+  // the offsets are on the host: validate them before any copy sized from them (header contract)
+  if (batch > 0) {
+    if (offsets_host[0] != 0 || offsets_host[batch] != n_total)
+      return fail(FV_ERR_ARG, "offsets[0] must be 0 and offsets[batch] == n_total");
+    for (int b = 0; b < batch; ++b)
+      if (offsets_host[b + 1] < offsets_host[b]) return fail(FV_ERR_ARG, "offsets must be non-decreasing (b=%d)", b);
+  }
   Layout L;
   if (!make_layout(n_total, batch, K, D, true, L, sc_in.n_cls)) return fail(FV_ERR_CUDA, "occupancy query failed");
   if (fv_status s = check_ws(ws, ws_bytes, L)) return s;
+  HostPipe *hp = nullptr;
+  if (fv_status s = host_pipe(hp)) return s;
   float *dX = (float *)at(ws, L.hx);
   int64_t *doff = (int64_t *)at(ws, L.hoff);
   float *dres = (float *)at(ws, L.hout);
@@ -559,26 +602,19 @@ fv_status encode_host_impl(const float *X_host, const int64_t *offsets_host, int
   if (!(flags & FV_PREPARED))
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
   if (batch == 0) return cudaStreamSynchronize(st) == cudaSuccess ? FV_OK : cuda_check("stream sync");
+  // the internal streams start behind everything already queued on the caller's stream (earlier work
+  // may still use the workspace bytes the X copies overwrite)
+  cudaEvent_t ev0 = hp->ev[2 * kHostChunks];
+  if (cudaEventRecord(ev0, st) != cudaSuccess || cudaStreamWaitEvent(hp->cin, ev0, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(hp->cout, ev0, 0) != cudaSuccess)
+    return cuda_check("order internal streams");
   // Pipelined in image chunks: the H2D copy of chunk k+1 (stream `cin`) and the D2H copy of chunk k-1
   // (stream `cout`) overlap the encode of chunk k on `stream`; events order each chunk's three steps.
   const size_t per_image = sc_in.n_cls > 0 ? (size_t)sc_in.n_cls : (size_t)2 * K * D;
-  const int nch = std::max(1, std::min(batch, 16));
-  cudaStream_t cin = nullptr, cout = nullptr;
-  cudaEvent_t ev[2 * 16] = {};
+  const int nch = std::max(1, std::min(batch, kHostChunks));
+  cudaStream_t cin = hp->cin, cout = hp->cout;
+  cudaEvent_t *ev = hp->ev;
   fv_status rs = FV_OK;
-  auto cleanup = [&]() {
-    for (auto &e : ev) if (e) cudaEventDestroy(e);
-    if (cin) cudaStreamDestroy(cin);
-    if (cout) cudaStreamDestroy(cout);
-  };
-  if (cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking) != cudaSuccess) {
-    rs = cuda_check("stream create");
-    cleanup();
-    return rs;
-  }
-  for (int k = 0; k < 2 * nch && rs == FV_OK; ++k)
-    if (cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming) != cudaSuccess) rs = cuda_check("event create");
   for (int k = 0; k < nch && rs == FV_OK; ++k) {
     const int b0 = (int)((int64_t)k * batch / nch), b1 = (int)((int64_t)(k + 1) * batch / nch);
     const int64_t r0 = offsets_host[b0], r1 = offsets_host[b1];
@@ -591,7 +627,7 @@ fv_status encode_host_impl(const float *X_host, const int64_t *offsets_host, int
     float *out = dres + (size_t)b0 * per_image;
     if (sc.n_cls > 0) { sc.scores = out; out = nullptr; }
     rs = encode_batched_impl(dX, doff + b0, b1 - b0, n_total, D, w, mu, sg, K, thr, flags | FV_PREPARED, out, ws,
-                             ws_bytes, st, &L, sc);
+                             ws_bytes, st, &L, sc, 0, b0);
     if (rs != FV_OK) break;
     cudaEventRecord(ev[2 * k + 1], st);
     cudaStreamWaitEvent(cout, ev[2 * k + 1], 0);
@@ -604,7 +640,6 @@ fv_status encode_host_impl(const float *X_host, const int64_t *offsets_host, int
   if (cudaStreamSynchronize(cout) != cudaSuccess || cudaStreamSynchronize(cin) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
     if (rs == FV_OK) rs = cuda_check("stream sync");
-  cleanup();
   return rs;
 }
 
@@ -922,6 +957,22 @@ fv_status fv_embed_encode_batched(const float *raw, const float *xy, const int64
     return s;
   return encode_batched_impl(Xe, offsets, batch, n_total, D, w, mu, sg, K, thr, flags, out, ws, ws_bytes, st, &L,
                              Scoring(), ldx);
+}
+
+fv_status fv_range_flags(const void *ws, size_t ws_bytes, int64_t n_total, int batch, int K, int D, int32_t *flags_out,
+                         fv_stream_t stream) {
+  g_launches = 0;
+  if (K < 1 || D < 1 || K > kMaxK || D > kDMax || n_total < 0 || batch < 0) return fail(FV_ERR_ARG, "bad sizes");
+  if (batch > 0 && !flags_out) return fail(FV_ERR_ARG, "null flags_out");
+  if (fv_status s = check_device()) return s;
+  Layout L;
+  if (!make_layout(n_total, batch, K, D, false, L)) return fail(FV_ERR_CUDA, "occupancy query failed");
+  if (fv_status s = check_ws(const_cast<void *>(ws), ws_bytes, L)) return s;
+  if (batch == 0) return FV_OK;
+  k_range_flags<<<(batch + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      (const int *)at(const_cast<void *>(ws), L.rflags), (const int *)at(const_cast<void *>(ws), L.gflag), batch, flags_out);
+  g_launches = 1;
+  return cuda_check("k_range_flags");
 }
 
 int fv_last_launch_count(void) { return g_launches; }

@@ -29,8 +29,9 @@ __device__ __forceinline__ double gmm_var(const float *sigmas, size_t i, bool st
 constexpr int kPrepThreads = 1024;
 __global__ void __launch_bounds__(kPrepThreads) k_prep_shift(const float *w, const float *mu, const float *sg, int K,
                                                            int D, int Kp, int stddev, double *cshift, float *xshift,
-                                                           float *xscale, double *pscale, double *xinv) {
+                                                           float *xscale, double *pscale, double *xinv, int *gflag) {
   __shared__ double s_w[kPrepThreads], s_m[kPrepThreads], s_q[kPrepThreads];
+  if (threadIdx.x == 0) *gflag = 0;  // k_prep_w (later on the stream) sets bit 1 for an fp16 overflow
   const int dstride = D <= kDP ? kDP : kDMax, ngrp = kPrepThreads / dstride;
   const int tid = threadIdx.x, k = tid % dstride, grp = tid / dstride;
   double ws = 0.0, am = 0.0, aq = 0.0;
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(512) k_prep_bias_final(int K, int Kp, const do
 //   coef[0][k][j] = mu_jk - c_k,  coef[1][k][j] = 1 / sqrt(var_jk),  coef[2][k][j] = 1 / var_jk
 // (Gaussian-fastest so the finalize reads them coalesced; zero for padded j / k).
 __global__ void k_prep_w(const float *mu, const float *sg, int K, int D, int stddev, const double *cshift,
-                         const float *xscale, uint8_t *wimg, double *coef, int wide) {
+                         const float *xscale, uint8_t *wimg, double *coef, int wide, int *gflag) {
   const int j = blockIdx.x, f = threadIdx.x, Kp = gridDim.x;
   int k, lin, off;
   if (!wide) {
@@ -158,11 +159,24 @@ __global__ void k_prep_w(const float *mu, const float *sg, int K, int D, int std
     coef[(size_t)(kDMax + k) * Kp + j] = 0.0;
     coef[(size_t)(2 * kDMax + k) * Kp + j] = 0.0;
   }
-  const float w32 = (float)wv;
+  float w32 = (float)wv;
+  // a coefficient outside the fp16 range (a standard deviation below ~RMS/150 in some dimension, or a
+  // non-finite / non-positive variance) cannot be split: it is stored as NaN, so every log-likelihood
+  // of every row is NaN and each image is flagged by k_stats; the GMM itself is flagged here (bit 1)
+  if (!(fabsf(w32) < 65504.f)) {
+    w32 = __int_as_float(0x7fffffff);
+    atomicOr(gflag, 2);
+  }
   const __half hi = __float2half_rn(w32);
   const __half lo = __float2half_rn(w32 - __half2float(hi));
   *reinterpret_cast<__half *>(wimg + off) = hi;
   *reinterpret_cast<__half *>(wimg + off + lo_off) = lo;
+}
+
+// fv_range_flags: flags_out[b] = rflags[b] | gflag (per-image range report of the last call).
+__global__ void k_range_flags(const int *rflags, const int *gflag, int batch, int *flags_out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < batch) flags_out[b] = rflags[b] | *gflag;
 }
 
 // Owner cluster of global tile t under the static split [c T / ncl, (c+1) T / ncl).
@@ -176,12 +190,12 @@ __device__ __forceinline__ int64_t tile_owner(int64_t t, int64_t T, int64_t ncl)
 // Also zeroes the finalize's per-image arrival counters (so no memset node separates k_stats from
 // k_finalize in the stream) and lets k_stats start its prologue early (programmatic launch).
 __global__ void k_schedule(const int64_t *offsets, int64_t *off1, int64_t n_single, int batch, int64_t *tile_start,
-                           int ncl, int *cstart, int *cown, unsigned *counters) {
+                           int ncl, int *cstart, int *cown, unsigned *counters, int *rflags) {
   __shared__ int64_t s_warp[32];
   __shared__ int64_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   ptx::griddep_launch_dependents();
-  for (int b = tid; b < batch; b += 1024) counters[b] = 0u;
+  for (int b = tid; b < batch; b += 1024) { counters[b] = 0u; rflags[b] = 0; }
   if (!offsets) {
     if (tid == 0) {
       off1[0] = 0; off1[1] = n_single;

@@ -93,6 +93,7 @@ struct Stats2Params {
   float *gamma_out;
   float *loglik_out;          // n_total (optional): per-descriptor log2 sum_j 2^(L_ij + b_j) (EM E-step)
   long long *trace;           // debug (GPUFV_TRACE builds): per-tile phase clocks of CTA 0
+  int *rflags;                // batch: range flags (bit 0: a row with non-finite log-likelihoods), zeroed by k_schedule
   int batch, D, K, Kp;
   int ldx;                    // row stride of X in floats (>= D, % 4 == 0)
   float threshold;
@@ -196,6 +197,16 @@ __device__ __forceinline__ void zr_box(const uint8_t *xbox, int row, int box, in
   tmem_st4(taddr + 32 + k0 / 2, qh);
   tmem_st4(taddr + 64 + k0 / 2, ll);
   tmem_st4(taddr + 96 + k0 / 2, ql);
+}
+
+// A row whose log-likelihoods are not all finite — a descriptor outside the fp16 operand range
+// (|x - c| >= ~256 RMS in some dimension: the squared feature overflows), a GMM coefficient outside it
+// (k_prep_w stores NaN), or non-finite input — has S = sum_j 2^(L_ij - M) NaN, 0 or inf (S >= 1
+// otherwise: the row maximum contributes 2^0).  Its posteriors are made NaN, so the image's statistics
+// and FV are NaN (never finite garbage), and the image is flagged for fv_range_flags.
+__device__ __forceinline__ void range_bad(const Stats2Params &p, int b, float &alpha_p, bool reporter) {
+  alpha_p = __int_as_float(0x7fffffff);
+  if (reporter && p.rflags) atomicOr(p.rflags + b, 1);
 }
 
 // WORK-warp wait on an MMA-completion barrier.  Every warp waits on its own (try_wait suspends the
@@ -554,6 +565,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       // this quarter's gamma_ij = e_ij 2^(m_h - M) / S; P = gamma 2^14
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
       if (row >= mt.nrows) alpha_p = 0.f;
+      else if (!(S > 0.5f && S < 3.0e38f)) range_bad(p, mt.b, alpha_p, h == 0 && rank == 0);
       TRW(6);
       // Zr(i+1) box 1: its TMA load started when box 0 was released above (a single 16 KB stage)
       if (i + 1 < n) conv_box(i + 1, 1);

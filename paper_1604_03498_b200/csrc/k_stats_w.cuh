@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       if (p.loglik_out && h == 0 && rank == 0 && row < mt.nrows) p.loglik_out[mt.row0 + row] = M + log2f(S);
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
       if (row >= mt.nrows) alpha_p = 0.f;
+      else if (!(S > 0.5f && S < 3.0e38f)) range_bad(p, mt.b, alpha_p, h == 0 && rank == 0);
       TRW(4);
 
       // ---- GEMM2(i-1) (both halves) done: S' chunk complete (fold), Z and P free

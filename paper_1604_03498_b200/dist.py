@@ -39,46 +39,75 @@ def partition_images(counts, world: int):
     return [sorted(p) for p in parts]
 
 
+def _all_gather(parts, t, group):
+    """all_gather; gloo has no CUDA all_gather, so CUDA tensors go through host copies there (tests run two
+    gloo ranks on one GPU; NCCL gathers device tensors directly)."""
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        host = [torch.empty(p.shape, dtype=p.dtype) for p in parts]
+        dist.all_gather(host, t.cpu(), group=group)
+        for p, h in zip(parts, host):
+            p.copy_(h)
+    else:
+        dist.all_gather(parts, t, group=group)
+
+
 def _rank_world(group):
     if dist.is_available() and dist.is_initialized():
         return dist.get_rank(group), dist.get_world_size(group)
     return 0, 1
 
 
-def encode_frames_sharded(X, offsets, gmm, threshold: float = 0.0, mode: int = 0, group=None, encode_fn=None,
-                          gather: bool = False):
-    """Frame-sharded encode: rank r encodes frames shard_ranges(B, world)[r].  X / offsets describe the
-    whole stream (offsets on the host); only this rank's rows are touched.  Returns this rank's FVs,
-    or all FVs in frame order when gather=True (an all_gather outside the hot path)."""
-    import numpy as np
+class FrameShard:
+    """This rank's share of a frame stream of B frames (CSR `offsets`, host): frames [lo, hi) =
+    shard_ranges(B, world)[rank], rows [r0, r1), and the frame offsets rebased to r0, built once as a
+    tensor on `device` (so a timed step makes no host->device copy)."""
 
+    def __init__(self, offsets, rank: int, world: int, device=None):
+        import numpy as np
+
+        off = np.asarray(offsets, dtype=np.int64)
+        self.B = off.shape[0] - 1
+        self.rank, self.world = rank, world
+        self.lo, self.hi = shard_ranges(self.B, world)[rank]
+        self.r0, self.r1 = int(off[self.lo]), int(off[self.hi])
+        self.sizes = [b - a for a, b in shard_ranges(self.B, world)]
+        self.local_offsets = torch.from_numpy(off[self.lo:self.hi + 1] - self.r0)
+        if device is not None:
+            self.local_offsets = self.local_offsets.to(device)
+
+
+def encode_frames_sharded(X, offsets, gmm, threshold: float = 0.0, mode: int = 0, group=None, encode_fn=None,
+                          gather: bool = False, shard: FrameShard | None = None, rows_local: bool = False):
+    """Frame-sharded encode: rank r encodes frames shard_ranges(B, world)[r].  X / offsets describe the
+    whole stream (offsets on the host), or, with rows_local=True, X holds only this rank's rows
+    [r0, r1) (each rank keeps just its own frames resident).  `shard` (a FrameShard) may be passed
+    instead of offsets to reuse a plan across steps.  Returns this rank's FVs, or all FVs in frame order
+    when gather=True (an all_gather outside the hot path)."""
     rank, world = _rank_world(group)
-    off = np.asarray(offsets, dtype=np.int64)
-    B = off.shape[0] - 1
-    lo, hi = shard_ranges(B, world)[rank]
-    r0, r1 = int(off[lo]), int(off[hi])
-    local_off = torch.from_numpy(off[lo:hi + 1] - r0)
+    if shard is None:
+        shard = FrameShard(offsets, rank, world)
+    Xs = X if rows_local else X[shard.r0:shard.r1]
     if encode_fn is None:
         from . import encode_batched as _enc
 
         def encode_fn(Xs, offs):
             return _enc(Xs, offs.to(Xs.device), gmm, threshold=threshold, mode=mode)
-    out = encode_fn(X[r0:r1], local_off)
+    out = encode_fn(Xs, shard.local_offsets)
     if not gather or world == 1:
         return out
-    sizes = [b - a for a, b in shard_ranges(B, world)]
-    mx = max(sizes)  # all_gather needs equal shapes: pad to the largest shard, trim after
+    mx = max(shard.sizes)  # all_gather needs equal shapes: pad to the largest shard, trim after
     padded = out.new_zeros((mx, out.shape[1]))
     padded[:out.shape[0]] = out
-    buf = [out.new_zeros((mx, out.shape[1])) for _ in sizes]
-    dist.all_gather(buf, padded, group=group)
-    return torch.cat([t[:s] for t, s in zip(buf, sizes)], 0)
+    buf = [out.new_zeros((mx, out.shape[1])) for _ in shard.sizes]
+    _all_gather(buf, padded, group)
+    return torch.cat([t[:s] for t, s in zip(buf, shard.sizes)], 0)
 
 
 def encode_descriptor_sharded(X_shard, gmm, threshold: float = 0.0, mode: int = 0, group=None, stats_fn=None,
-                              finalize_fn=None, deterministic: bool = False):
+                              finalize_fn=None, deterministic: bool = False, return_stats: bool = False):
     """One descriptor set sharded over ranks: X_shard is this rank's contiguous rows.  Returns the
-    (identical on every rank) normalised FV of the whole set, shape (2KD,)."""
+    (identical on every rank) normalised FV of the whole set, shape (2KD,) — and, with return_stats, the
+    all-reduced statistics [N, S0, S1, S2] (1, 1 + K(2D+1)) as well."""
     rank, world = _rank_world(group)
     if stats_fn is None:
         from . import stats_batched as _stats
@@ -91,17 +120,20 @@ def encode_descriptor_sharded(X_shard, gmm, threshold: float = 0.0, mode: int = 
 
         def finalize_fn(st):
             return _fin(st, gmm, mode=mode)
-    st = stats_fn(X_shard).reshape(1, -1).to(torch.float64)  # [N, S0, S1, S2] (a6)
+    st = stats_fn(X_shard).reshape(1, -1)  # [N, S0, S1, S2] (a6)
+    if st.dtype != torch.float64:
+        st = st.to(torch.float64)
     if world > 1:
         if deterministic:
             parts = [torch.empty_like(st) for _ in range(world)]
-            dist.all_gather(parts, st, group=group)
+            _all_gather(parts, st, group)
             st = parts[0].clone()
             for t in parts[1:]:
                 st += t  # fixed rank order
         else:
             dist.all_reduce(st, op=dist.ReduceOp.SUM, group=group)  # a8
-    return finalize_fn(st).reshape(-1)
+    fv = finalize_fn(st).reshape(-1)
+    return (fv, st) if return_stats else fv
 
 
 def em_step_sharded(X_shard, gmm, group=None, estep_fn=None, mstep_fn=None, deterministic: bool = False,
@@ -126,7 +158,7 @@ def em_step_sharded(X_shard, gmm, group=None, estep_fn=None, mstep_fn=None, dete
     if world > 1:
         if deterministic:
             parts = [torch.empty_like(buf) for _ in range(world)]
-            dist.all_gather(parts, buf, group=group)
+            _all_gather(parts, buf, group)
             buf = parts[0].clone()
             for t in parts[1:]:
                 buf += t  # fixed rank order
@@ -136,30 +168,26 @@ def em_step_sharded(X_shard, gmm, group=None, estep_fn=None, mstep_fn=None, dete
 
 
 def score_frames_sharded(X, offsets, gmm, svm_w, svm_b=None, threshold: float = 0.0, mode: int = 0, group=None,
-                         score_fn=None, gather: bool = True):
+                         score_fn=None, gather: bool = True, shard: FrameShard | None = None, rows_local: bool = False):
     """Frame-sharded monitoring (NEXT-4): rank r scores frames shard_ranges(B, world)[r] with
     the classifier fused into the finalize (no FV leaves the GPU); only the (frames, n_cls) scores are
-    all-gathered (4 B per frame and class instead of 2KD floats)."""
-    import numpy as np
-
+    all-gathered (4 B per frame and class instead of 2KD floats).  X / shard / rows_local as in
+    encode_frames_sharded."""
     rank, world = _rank_world(group)
-    off = np.asarray(offsets, dtype=np.int64)
-    B = off.shape[0] - 1
-    lo, hi = shard_ranges(B, world)[rank]
-    r0, r1 = int(off[lo]), int(off[hi])
-    local_off = torch.from_numpy(off[lo:hi + 1] - r0)
+    if shard is None:
+        shard = FrameShard(offsets, rank, world)
+    Xs = X if rows_local else X[shard.r0:shard.r1]
     if score_fn is None:
         from . import encode_scored_batched as _sc
 
         def score_fn(Xs, offs):
             return _sc(Xs, offs.to(Xs.device), gmm, svm_w, svm_b, threshold=threshold, mode=mode)
-    s = score_fn(X[r0:r1], local_off)
+    s = score_fn(Xs, shard.local_offsets)
     if not gather or world == 1:
         return s
-    sizes = [b - a for a, b in shard_ranges(B, world)]
-    mx = max(sizes)
+    mx = max(shard.sizes)
     padded = s.new_zeros((mx, s.shape[1]))
     padded[:s.shape[0]] = s
-    buf = [s.new_zeros((mx, s.shape[1])) for _ in sizes]
-    dist.all_gather(buf, padded, group=group)
-    return torch.cat([t[:n] for t, n in zip(buf, sizes)], 0)
+    buf = [s.new_zeros((mx, s.shape[1])) for _ in shard.sizes]
+    _all_gather(buf, padded, group)
+    return torch.cat([t[:n] for t, n in zip(buf, shard.sizes)], 0)
