@@ -60,7 +60,9 @@ enum {
   FV_NORM_MASK = 3,
   FV_SIGMA_IS_STDDEV = 1u << 4, /* `sigmas` are standard deviations (default: variances, A1)    */
   FV_DETERMINISTIC = 1u << 5,   /* accepted for compatibility; every path is deterministic        */
-  FV_PREPARED = 1u << 6         /* `ws` already holds this GMM prepared by fv_gmm_prepare: skip a1 */
+  FV_PREPARED = 1u << 6,        /* `ws` already holds this GMM prepared by fv_gmm_prepare: skip a1 */
+  FV_DENSE_STATS = 1u << 7      /* threshold > 0: accumulate with the dense tensor-core GEMM2 instead of
+                                   the survivor path (Alg. 5 early termination, D <= 64) */
 };
 
 /* Bytes of device workspace needed by the calls below for this problem size.  n_total = total

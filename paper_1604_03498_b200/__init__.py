@@ -13,7 +13,7 @@ import os
 import torch
 
 __all__ = [
-    "NORM_IMPROVED", "NORM_POWER_L2", "NORM_NONE", "SIGMA_IS_STDDEV", "PREPARED",
+    "NORM_IMPROVED", "NORM_POWER_L2", "NORM_NONE", "SIGMA_IS_STDDEV", "PREPARED", "DENSE_STATS",
     "GMM", "Workspace", "lib", "lib_path", "workspace_bytes", "gmm_prepare", "encode", "encode_batched",
     "encode_batched_host", "stats_batched", "finalize", "posteriors", "last_launch_count", "profile_events",
     "encode_scored_batched", "encode_scored_batched_host", "MAX_CLASSES", "gmm_estep", "gmm_mstep", "gmm_em_step",
@@ -26,6 +26,7 @@ NORM_NONE = 2
 SIGMA_IS_STDDEV = 1 << 4
 DETERMINISTIC = 1 << 5
 PREPARED = 1 << 6
+DENSE_STATS = 1 << 7  # threshold > 0: dense tensor-core GEMM2 instead of the survivor (Alg. 5) path
 _RAW_LOGLIK = 1 << 8
 MAX_CLASSES = 32  # test hook of fv_posteriors: raw log2-likelihoods instead of gamma
 

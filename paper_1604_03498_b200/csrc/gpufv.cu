@@ -22,6 +22,7 @@
 #include "k_aux.cuh"
 #include "k_stats.cuh"
 #include "k_stats_w.cuh"
+#include "k_stats_sp.cuh"
 #include "k_embed.cuh"
 
 using namespace gpufv;
@@ -92,7 +93,9 @@ int num_clusters(int C, bool wide) {
   if (cudaFuncSetAttribute(k_stats<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess)
+      cudaFuncSetAttribute(k_stats_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_sp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSpBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_sp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSpBytes) != cudaSuccess)
     return -1;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -200,7 +203,7 @@ fv_status check_gmm_args(int K, int D, const float *w, const float *mu, const fl
   if (K > kMaxK) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kMaxK);
   if (D > kDMax) return fail(FV_ERR_UNSUPPORTED, "D=%d > %d", D, kDMax);
   if (need_d4 && D % 4 != 0) return fail(FV_ERR_UNSUPPORTED, "D=%d is not a multiple of 4 (pad, reading A13)", D);
-  const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED;
+  const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED | FV_DENSE_STATS;
   if (flags & ~known) return fail(FV_ERR_ARG, "unknown flag bits 0x%x", flags & ~known);
   if ((flags & FV_NORM_MASK) == 3) return fail(FV_ERR_ARG, "invalid normalisation mode 3");
   return FV_OK;
@@ -246,7 +249,8 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
 // a2-a6 over a batch: schedule + persistent stats kernel.  gamma (optional) for fv_posteriors.
 fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets, int64_t n_single, int batch, int D,
                        int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st,
-                       float *loglik_rows = nullptr, int ldx = 0, int rf_base = 0) {
+                       float *loglik_rows = nullptr, int ldx = 0, int rf_base = 0, int64_t rows = -1,
+                       bool dense = false) {
   if (ldx <= 0) ldx = D;
   int *rflags = (int *)at(ws, L.rflags) + rf_base;
   // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
@@ -270,6 +274,8 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.loglik_out = loglik_rows;
   p.trace = g_trace;
   p.rflags = rflags;
+  if (rows < 0) rows = n_single;  // rows of this launch's images (n_total unless a host-pipeline chunk)
+  p.kfold = (batch > 0 && rows / batch >= kLongSetRows) ? kFoldLong : kFold;
   p.batch = batch;
   p.D = D;
   p.K = K;
@@ -277,6 +283,9 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.ldx = ldx;
   p.threshold = thr > 0.f ? thr : 0.f;
   p.gamma_mode = gamma_mode;
+  // tau > 0 on the narrow family: the survivor (Alg. 5) path, unless the caller forces the dense GEMM2
+  // (FV_DENSE_STATS) or needs per-row outputs (posteriors / log-likelihoods: dense kernel only)
+  const bool sparse = !is_wide(K, D) && p.threshold > 0.f && !dense && !gamma && !loglik_rows;
   // X as a 2-D tensor map: dims {D, n_total}, boxes of 32 floats x 128 rows, 128B swizzle; rows past
   // n_total and dims past D read as zero.
   CUtensorMap tmap;
@@ -291,13 +300,16 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
     }
     cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(L.n_total > 0 ? L.n_total : 1)};
     cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
-    cuuint32_t box[2] = {32, 128};
+    // the survivor kernel takes one unswizzled box of kSpXLd floats x 128 rows per tile, the dense
+    // kernels two 128B-swizzled boxes of 32 floats
+    cuuint32_t box[2] = {sparse ? (cuuint32_t)kSpXLd : 32u, 128};
     cuuint32_t estr[2] = {1, 1};
     // an empty launch (n_total == 0, X typically NULL) loads no tile, but the map still needs a valid
     // global address: point it at the workspace
     float *xmap = (X && L.n_total > 0) ? const_cast<float *>(X) : reinterpret_cast<float *>(ws);
     CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, xmap, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sparse ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(FV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   }
@@ -311,13 +323,14 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3(L.C * L.ncl, 1, 1);
   cfg.blockDim = dim3(kThreads2, 1, 1);
-  cfg.dynamicSmemBytes = is_wide(K, D) ? kSmemWBytes : kSmem2Bytes;
+  cfg.dynamicSmemBytes = is_wide(K, D) ? kSmemWBytes : sparse ? kSmemSpBytes : kSmem2Bytes;
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   if (g_prof_start) cudaEventRecord(g_prof_start, st);
   cudaError_t e;
-  if (!is_wide(K, D)) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false>, tmap, p);
+  if (sparse) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats_sp<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_sp<false>, tmap, p);
+  else if (!is_wide(K, D)) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false>, tmap, p);
   else e = (D == kDMax) ? cudaLaunchKernelEx(&cfg, k_stats_w<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false>, tmap, p);
   if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
   g_launches += 1;
@@ -461,7 +474,8 @@ struct Scoring {
 fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D,
                               const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
                               float *out, void *ws, size_t ws_bytes, cudaStream_t st, const Layout *Lin,
-                              const Scoring &sc = Scoring(), int ldx = 0, int rf_base = 0) {
+                              const Scoring &sc = Scoring(), int ldx = 0, int rf_base = 0, int64_t rows = -1) {
+  const bool dense = (flags & FV_DENSE_STATS) != 0;
   Layout L;
   if (Lin) L = *Lin;
   else if (!make_layout(n_total, batch, K, D, false, L, sc.n_cls)) return fail(FV_ERR_CUDA, "occupancy query failed");
@@ -469,7 +483,8 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   if (!(flags & FV_PREPARED))
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
   if (batch == 0) return FV_OK;
-  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx, rf_base))
+  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx, rf_base, rows,
+                                 dense))
     return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   f.out = out;
@@ -627,7 +642,7 @@ fv_status encode_host_impl(const float *X_host, const int64_t *offsets_host, int
     float *out = dres + (size_t)b0 * per_image;
     if (sc.n_cls > 0) { sc.scores = out; out = nullptr; }
     rs = encode_batched_impl(dX, doff + b0, b1 - b0, n_total, D, w, mu, sg, K, thr, flags | FV_PREPARED, out, ws,
-                             ws_bytes, st, &L, sc, 0, b0);
+                             ws_bytes, st, &L, sc, 0, b0, r1 - r0);
     if (rs != FV_OK) break;
     cudaEventRecord(ev[2 * k + 1], st);
     cudaStreamWaitEvent(cout, ev[2 * k + 1], 0);
@@ -710,7 +725,9 @@ fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, in
   if (!(flags & FV_PREPARED))
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
   if (batch == 0) return FV_OK;
-  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st)) return s;
+  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, 0, 0, -1,
+                                 (flags & FV_DENSE_STATS) != 0))
+    return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   f.stats_out = stats;
   for (int b0 = 0; b0 < batch; b0 += 65535) {

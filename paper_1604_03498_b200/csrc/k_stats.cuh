@@ -93,6 +93,7 @@ struct Stats2Params {
   float *gamma_out;
   float *loglik_out;          // n_total (optional): per-descriptor log2 sum_j 2^(L_ij + b_j) (EM E-step)
   long long *trace;           // debug (GPUFV_TRACE builds): per-tile phase clocks of CTA 0
+  int kfold;                  // GEMM2 restart period in tiles (kFold, or kFoldLong for large sets)
   int *rflags;                // batch: range flags (bit 0: a row with non-finite log-likelihoods), zeroed by k_schedule
   int batch, D, K, Kp;
   int ldx;                    // row stride of X in floats (>= D, % 4 == 0)
@@ -129,8 +130,9 @@ struct TileWalker {
     const int rem = off_b1 - m.row0;
     m.nrows = rem < kTileM ? rem : kTileM;
     const bool seg_last = (t + 1 == t1) || (t + 1 >= ts_b1);
-    m.flags = (seg_last ? 1 : 0) | ((seg_pos % kFold) == 0 ? 2 : 0) | (seg_pos == 0 ? 8 : 0) |
-              ((seg_last || (seg_pos + 1) % kFold == 0) ? 4 : 0);
+    const int kf = p->kfold;
+    m.flags = (seg_last ? 1 : 0) | ((seg_pos % kf) == 0 ? 2 : 0) | (seg_pos == 0 ? 8 : 0) |
+              ((seg_last || (seg_pos + 1) % kf == 0) ? 4 : 0);
     return m;
   }
   __device__ void next() {

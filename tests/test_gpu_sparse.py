@@ -1,0 +1,99 @@
+"""NEXT-1: the thresholded statistics through the survivor path (Alg. 5's early termination, PAPER.md:366-371,
+P:415-442; csrc/k_stats_sp.cuh) against the oracle in the same mode, and against the dense tensor-core
+GEMM2 (FV_DENSE_STATS) on the same inputs.  Both include exactly the pairs gamma > tau (Alg.1 l.18), so
+they agree to rounding; the survivor path accumulates in round-to-nearest fp32, so it is at least as close
+to the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import fvgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+FV_RTOL = 1e-4
+TAU = 1e-6
+
+
+@pytest.fixture(scope="module")
+def fv():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1604_03498_b200 as m
+    return m
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("K,D", [(256, 64), (128, 64), (16, 64), (200, 32), (256, 36), (64, 4), (1, 64)])
+@pytest.mark.parametrize("tau", [1e-6, 1e-3, 0.2])
+def test_sparse_matches_oracle_and_dense(fv, K, D, tau):
+    gmm_np = fvgen.make_gmm(K, D, seed=61 + K + D)
+    counts = [0, 1, 127, 128, 129, 3000, 5000, 0, 777]
+    X, off = fvgen.make_batch(gmm_np, counts, seed_base=62)
+    gmm = fv.GMM(*gmm_np)
+    sp = fv.encode_batched(dev(X), dev(off), gmm, threshold=tau).cpu().numpy()
+    sp2 = fv.encode_batched(dev(X), dev(off), gmm, threshold=tau).cpu().numpy()
+    assert np.array_equal(sp, sp2)  # fixed summation order: bitwise repeatable
+    de = fv.encode_batched(dev(X), dev(off), gmm, threshold=tau, mode=fv.NORM_IMPROVED | fv.DENSE_STATS).cpu().numpy()
+    ref = oracle.encode_batched(X, off, *gmm_np, threshold=tau)
+    for b, n in enumerate(counts):
+        if n == 0:
+            assert np.all(sp[b] == 0)
+            continue
+        assert rel_l2(sp[b], ref[b]) <= FV_RTOL, (b, rel_l2(sp[b], ref[b]))
+        assert rel_l2(de[b], ref[b]) <= FV_RTOL, (b, rel_l2(de[b], ref[b]))
+        # the survivor path sums the same pairs in round-to-nearest fp32: never further from the oracle
+        # than the dense split-fp16 GEMM2 by more than rounding
+        assert rel_l2(sp[b], ref[b]) <= rel_l2(de[b], ref[b]) + 2e-6, b
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_sparse_all_modes_and_stats(fv, mode):
+    gmm_np = fvgen.make_gmm(256, 64, seed=63)
+    X, off = fvgen.make_batch(gmm_np, [4000, 2500, 9000], seed_base=64)
+    gmm = fv.GMM(*gmm_np)
+    out = fv.encode_batched(dev(X), dev(off), gmm, threshold=TAU, mode=mode).cpu().numpy()
+    ref = oracle.encode_batched(X, off, *gmm_np, threshold=TAU, mode=mode)
+    for b in range(3):
+        assert rel_l2(out[b], ref[b]) <= FV_RTOL
+    st = fv.stats_batched(dev(X), dev(off), gmm, threshold=TAU).cpu().numpy()
+    rs = oracle.stats_batched(X, off, *gmm_np, threshold=TAU)
+    K = 256
+    for b in range(3):
+        assert st[b, 0] == rs[b, 0]
+        assert rel_l2(st[b, 1:1 + K], rs[b, 1:1 + K]) <= 1e-6
+        assert rel_l2(st[b, 1 + K:], rs[b, 1 + K:]) <= 1e-6
+
+
+def test_sparse_c4_frames_and_scoring(fv):
+    """The C4 launch shape (512 frames x 5000 here) through the survivor path, with the fused scoring."""
+    gmm_np = fvgen.make_gmm(256, 64, seed=1604)
+    F, P = 512, 5000
+    X = fvgen.make_frames(gmm_np, F, P, seed=1604 + 20000)
+    off = np.arange(F + 1, dtype=np.int64) * P
+    gmm = fv.GMM(*gmm_np)
+    out = fv.encode_batched(dev(X), dev(off), gmm, threshold=TAU).cpu().numpy()
+    for f in (0, 1, 255, 511):
+        assert rel_l2(out[f], oracle.encode(X[f * P:(f + 1) * P], *gmm_np, threshold=TAU)) <= FV_RTOL
+    W = np.random.default_rng(65).standard_normal((2, 2 * 256 * 64)).astype(np.float32)
+    sc = fv.encode_scored_batched(dev(X), dev(off), gmm, dev(W), threshold=TAU).cpu().numpy()
+    np.testing.assert_allclose(sc, out.astype(np.float64) @ W.T.astype(np.float64), rtol=0, atol=1e-4 * np.linalg.norm(W, axis=1).max())
+
+
+def test_sparse_flat_posteriors(fv):
+    """The f = 0.15 stress GMM (~81 survivors per descriptor): slower, still exact."""
+    gmm_np = fvgen.make_gmm(256, 64, seed=66, f=0.15)
+    X, off = fvgen.make_batch(gmm_np, [6000, 300], seed_base=67)
+    out = fv.encode_batched(dev(X), dev(off), fv.GMM(*gmm_np), threshold=TAU).cpu().numpy()
+    ref = oracle.encode_batched(X, off, *gmm_np, threshold=TAU)
+    assert max(rel_l2(out[b], ref[b]) for b in range(2)) <= FV_RTOL
