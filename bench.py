@@ -286,7 +286,7 @@ def load_peaks():
         return {}
 
 
-def run_legs(fv, gmm, gmm_np, dev, stream, rank, world):
+def run_legs(fv, gmm, gmm_np, dev, stream, rank, world, Xd_c4=None, offs_c4=None):
     """The other BASELINE configs as legs of the default run (device-timed, CUDA events, max over ranks):
     C3 (configs[2]): a VOC2007-shaped ragged batch of 256 images x round(20000 U(0.75, 1.25)) descriptors
        per rank, tau = 1e-6, one fv_encode_batched call (this batch size takes the whole-image finalize);
@@ -342,6 +342,29 @@ def run_legs(fv, gmm, gmm_np, dev, stream, rank, world):
     def one():
         fv.encode(x1, g1, ws=ws1, prepared=True, out=o1)
 
+    # NEXT-1 A/B: the same C4 launch (its first 1024 frames) through the survivor path (FV_SPARSE_STATS)
+    # against the default dense GEMM2, device-timed back to back
+    if Xd_c4 is not None:
+        nf = min(1024, offs_c4.shape[0] - 1)
+        xa, oa = Xd_c4[:nf * PER_FRAME], offs_c4[:nf + 1]
+        wsa = fv.Workspace(device=dev)
+        wsa.ensure(fv.workspace_bytes(xa.shape[0], nf, K, D))
+        fv.gmm_prepare(gmm, wsa)
+        oo = torch.empty(nf, 2 * K * D, dtype=torch.float32, device=dev)
+        ab = {}
+        for name, mode in (("dense", 0), ("sparse", fv.SPARSE_STATS)):
+            for _ in range(2):
+                fv.encode_batched(xa, oa, gmm, threshold=TAU, mode=mode, ws=wsa, prepared=True, out=oo)
+            a.record(stream)
+            for _ in range(5):
+                fv.encode_batched(xa, oa, gmm, threshold=TAU, mode=mode, ws=wsa, prepared=True, out=oo)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            msx = a.elapsed_time(b) / 5
+            ab[name] = {"ms_per_step": msx, "value": xa.shape[0] / (msx * 1e-3), "unit": UNIT}
+        ab["workload"] = f"C4 first {nf} frames x {PER_FRAME}, tau={TAU}; dense GEMM2 vs FV_SPARSE_STATS survivor path"
+        legs["next1_ab"] = ab
+        del wsa, oo
     legs["c1"] = {"eager_us": latency_us(one, dev, stream)}
     legs["c1"]["graph_us"] = graph_latency_us(one, dev, stream)
     legs["c1"]["workload"] = f"C1: one image, {c1['counts'][0]} descriptors, K={c1['K']}, D={c1['D']}, exact"
@@ -1029,7 +1052,7 @@ def main():
 
     legs = None
     if not args.no_legs:
-        legs = run_legs(fv, gmm, gmm_np, dev, stream, rank, world)
+        legs = run_legs(fv, gmm, gmm_np, dev, stream, rank, world, Xd, offd)
 
     cpu = None
     stress = None

@@ -61,8 +61,10 @@ enum {
   FV_SIGMA_IS_STDDEV = 1u << 4, /* `sigmas` are standard deviations (default: variances, A1)    */
   FV_DETERMINISTIC = 1u << 5,   /* accepted for compatibility; every path is deterministic        */
   FV_PREPARED = 1u << 6,        /* `ws` already holds this GMM prepared by fv_gmm_prepare: skip a1 */
-  FV_DENSE_STATS = 1u << 7      /* threshold > 0: accumulate with the dense tensor-core GEMM2 instead of
-                                   the survivor path (Alg. 5 early termination, D <= 64) */
+  FV_SPARSE_STATS = 1u << 7     /* threshold > 0, D <= 64, K <= 256: accumulate only the pairs gamma > tau
+                                   on the CUDA cores (Alg. 5 early termination, round-to-nearest fp32 sums)
+                                   instead of the dense tensor-core GEMM2; same result to rounding, slower
+                                   on the acceptance generator */
 };
 
 /* Bytes of device workspace needed by the calls below for this problem size.  n_total = total

@@ -13,7 +13,7 @@ import os
 import torch
 
 __all__ = [
-    "NORM_IMPROVED", "NORM_POWER_L2", "NORM_NONE", "SIGMA_IS_STDDEV", "PREPARED", "DENSE_STATS",
+    "NORM_IMPROVED", "NORM_POWER_L2", "NORM_NONE", "SIGMA_IS_STDDEV", "PREPARED", "SPARSE_STATS",
     "GMM", "Workspace", "lib", "lib_path", "workspace_bytes", "gmm_prepare", "encode", "encode_batched",
     "encode_batched_host", "stats_batched", "finalize", "posteriors", "last_launch_count", "profile_events",
     "encode_scored_batched", "encode_scored_batched_host", "MAX_CLASSES", "gmm_estep", "gmm_mstep", "gmm_em_step",
@@ -26,7 +26,7 @@ NORM_NONE = 2
 SIGMA_IS_STDDEV = 1 << 4
 DETERMINISTIC = 1 << 5
 PREPARED = 1 << 6
-DENSE_STATS = 1 << 7  # threshold > 0: dense tensor-core GEMM2 instead of the survivor (Alg. 5) path
+SPARSE_STATS = 1 << 7  # threshold > 0: survivor (Alg. 5) accumulation instead of the dense tensor-core GEMM2
 _RAW_LOGLIK = 1 << 8
 MAX_CLASSES = 32  # test hook of fv_posteriors: raw log2-likelihoods instead of gamma
 
@@ -252,7 +252,7 @@ def encode_batched_host(X_host, offsets_host, gmm: GMM, threshold: float = 0.0, 
 
 
 def stats_batched(X, offsets, gmm: GMM, threshold: float = 0.0, ws: Workspace | None = None,
-                  prepared: bool = False, out=None):
+                  prepared: bool = False, out=None, sparse: bool = False):
     """Sufficient statistics (batch, 1 + K(2D+1)) float64 about c (reading A19); they add across
     disjoint descriptor shards."""
     _check_X(X, gmm.D)
@@ -264,7 +264,8 @@ def stats_batched(X, offsets, gmm: GMM, threshold: float = 0.0, ws: Workspace | 
         out = torch.empty(B, 1 + gmm.K * (2 * gmm.D + 1), dtype=torch.float64, device=X.device)
     w, m, s = gmm.ptrs()
     _check(lib.fv_stats_batched(_ptr(X), _ptr(offsets), B, X.shape[0], gmm.D, w, m, s, gmm.K, float(threshold),
-                                _mode_flags(gmm, 0, prepared), _ptr(out), *ws.args(), _stream()))
+                                _mode_flags(gmm, SPARSE_STATS if sparse else 0, prepared), _ptr(out), *ws.args(),
+                                _stream()))
     return out
 
 

@@ -203,7 +203,7 @@ fv_status check_gmm_args(int K, int D, const float *w, const float *mu, const fl
   if (K > kMaxK) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kMaxK);
   if (D > kDMax) return fail(FV_ERR_UNSUPPORTED, "D=%d > %d", D, kDMax);
   if (need_d4 && D % 4 != 0) return fail(FV_ERR_UNSUPPORTED, "D=%d is not a multiple of 4 (pad, reading A13)", D);
-  const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED | FV_DENSE_STATS;
+  const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED | FV_SPARSE_STATS;
   if (flags & ~known) return fail(FV_ERR_ARG, "unknown flag bits 0x%x", flags & ~known);
   if ((flags & FV_NORM_MASK) == 3) return fail(FV_ERR_ARG, "invalid normalisation mode 3");
   return FV_OK;
@@ -250,7 +250,7 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
 fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets, int64_t n_single, int batch, int D,
                        int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st,
                        float *loglik_rows = nullptr, int ldx = 0, int rf_base = 0, int64_t rows = -1,
-                       bool dense = false) {
+                       bool sparse_req = false) {
   if (ldx <= 0) ldx = D;
   int *rflags = (int *)at(ws, L.rflags) + rf_base;
   // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
@@ -283,9 +283,9 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.ldx = ldx;
   p.threshold = thr > 0.f ? thr : 0.f;
   p.gamma_mode = gamma_mode;
-  // tau > 0 on the narrow family: the survivor (Alg. 5) path, unless the caller forces the dense GEMM2
-  // (FV_DENSE_STATS) or needs per-row outputs (posteriors / log-likelihoods: dense kernel only)
-  const bool sparse = !is_wide(K, D) && p.threshold > 0.f && !dense && !gamma && !loglik_rows;
+  // FV_SPARSE_STATS with tau > 0 on the narrow family: the survivor (Alg. 5) path instead of the dense
+  // GEMM2 (measured 1.8x slower on C4: opt-in); per-row outputs need the dense kernel
+  const bool sparse = sparse_req && !is_wide(K, D) && p.threshold > 0.f && !gamma && !loglik_rows;
   // X as a 2-D tensor map: dims {D, n_total}, boxes of 32 floats x 128 rows, 128B swizzle; rows past
   // n_total and dims past D read as zero.
   CUtensorMap tmap;
@@ -475,7 +475,7 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
                               const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
                               float *out, void *ws, size_t ws_bytes, cudaStream_t st, const Layout *Lin,
                               const Scoring &sc = Scoring(), int ldx = 0, int rf_base = 0, int64_t rows = -1) {
-  const bool dense = (flags & FV_DENSE_STATS) != 0;
+  const bool sparse = (flags & FV_SPARSE_STATS) != 0;
   Layout L;
   if (Lin) L = *Lin;
   else if (!make_layout(n_total, batch, K, D, false, L, sc.n_cls)) return fail(FV_ERR_CUDA, "occupancy query failed");
@@ -484,7 +484,7 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
   if (batch == 0) return FV_OK;
   if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx, rf_base, rows,
-                                 dense))
+                                 sparse))
     return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   f.out = out;
@@ -726,7 +726,7 @@ fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, in
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
   if (batch == 0) return FV_OK;
   if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, 0, 0, -1,
-                                 (flags & FV_DENSE_STATS) != 0))
+                                 (flags & FV_SPARSE_STATS) != 0))
     return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   f.stats_out = stats;

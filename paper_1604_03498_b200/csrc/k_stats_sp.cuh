@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_sp(const __grid_constant
       const uint64_t dW = desc_sw128(sW, 16, 1024);
       mbar_wait(&bars[S_W_FULL], 0);
       for (int i = 0; i < n; ++i) {
+        TR(12);
         mbar_wait(&bars[S_ZR_FULL], i & 1);
+        TR(13);
         if (i >= 2) mbar_wait(&bars[S_LE0 + (i & 1)], ((i - 2) >> 1) & 1);  // L[i % 2] read by softmax(i-2)
         tc_fence_after();
         const uint32_t zr = tmem + kSpTZr + 128 * (i & 1), dl = tmem + kSpTL + 128 * (i & 1);
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_sp(const __grid_constant
           }
         }
         mma_commit_w(&bars[S_G1D0 + (i & 1)]);
+        TR(14);
       }
     }
   } else {
@@ -254,7 +257,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_sp(const __grid_constant
       zr_done();
     }
     for (int i = 0; i < n; ++i) {
+      TRW(0);
       work_wait(&bars[S_G1D0 + (i & 1)], (i >> 1) & 1);  // L(i) ready
+      TRW(1);
       float v[32];
       {
         uint32_t rr[32];
@@ -266,6 +271,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_sp(const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[S_LE0 + (i & 1)]);
+      TRW(2);
       const TileMeta mt = s_meta[i & 3];
       float m = -3.0e38f;
 #pragma unroll
@@ -302,16 +308,20 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_sp(const __grid_constant
         // tile i+1 (resident since tile i-1 was accumulated): box 0 inside the MUFU-bound exp loop,
         // box 1 behind the exchange send; then GEMM1(i+1) may start
         mbar_wait(&bars[S_XFULL0 + ((i + 1) & 1)], ((i + 1) >> 1) & 1);
+        TRW(3);
         const float ssum = exp_local();
         conv_box(i + 1, 0);
         send(ssum);
+        TRW(4);
         conv_box(i + 1, 1);
         zr_done();
+        TRW(5);
       } else {
         send(exp_local());
       }
       if (C > 1) mbar_wait(&bars[S_XCHG0 + par], (i >> 1) & 1);
       else named_bar_sync(kBarXchgLocal, kWarpsWork * 32);
+      TRW(6);
       float M = -3.0e38f, S = 0.f;
       {
         float2 o[kMaxC2 * 4];
@@ -329,6 +339,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_sp(const __grid_constant
 
       // ---- a4': Gamma row (gamma 2^14, all 32 columns) and the survivor bits gamma > tau (a NaN row
       // counts as surviving, so a flagged row reaches the statistics as NaN)
+      TRW(7);
       uint32_t sbits = 0;
       {
         const float2 ap = make_float2(alpha_p, alpha_p);
@@ -346,7 +357,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_sp(const __grid_constant
       }
       if (row >= mt.nrows) sbits = 0u;  // rows past the image end never enter the sums
       s_mask[(32 * h + lane) * 4 + q] = warp_bit_transpose(sbits, lane);  // Gaussian 32h + lane, rows 32q..
+      TRW(8);
       named_bar_sync(kBarSpG, kWarpsWork * 32);
+      TRW(9);
 
       // ---- a5': survivors of this warp's 8 Gaussians, rows ascending, into fp32 registers.  Per
       // Gaussian the warp first compacts the mask into a row list (lane l places rows 32q + l), then
@@ -393,7 +406,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_sp(const __grid_constant
           __syncwarp();  // the list is rewritten for the next Gaussian
         }
       }
+      TRW(10);
       named_bar_sync(kBarSpA, kWarpsWork * 32);  // Gamma, masks and X(i) are free
+      TRW(11);
       if (ww == 0 && lane == 0) mbar_arrive(&bars[S_XEMPTY0 + (i & 1)]);
 
       // ---- a6: chunk end -> segment slot (first chunk stores, later chunks add, same thread, in order)
