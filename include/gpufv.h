@@ -191,9 +191,12 @@ fv_status fv_gmm_em_step(const float *X, int64_t N, int D, const float *weights,
  *   X_out[i * ldx + m] = xy[2 i] / img_wh[2 b],  X_out[i * ldx + m + 1] = xy[2 i + 1] / img_wh[2 b + 1]
  *   X_out[i * ldx + c] = 0 for m + 2 <= c < ldx,
  * for descriptor i of image b (rows offsets[b] .. offsets[b+1]-1).  raw: device, n_total x 128 fp32
- * (16-byte aligned); xy: n_total x 2 keypoint pixel coordinates in the original image; img_wh: batch x
- * 2 (width, height); pca_mean: 128; pca_basis: m x 128 row-major (rows orthonormal: not checked);
- * 1 <= m <= 126; ldx >= m + 2, ldx % 4 == 0.  fp32 accumulation in k = 0..127 order. */
+ * (16-byte aligned); xy: n_total x 2 keypoint pixel coordinates in the original image (16-byte
+ * aligned); img_wh: batch x 2 (width, height; 8-byte aligned); pca_mean: 128 (16-byte aligned);
+ * pca_basis: m x 128 row-major (rows orthonormal: not checked); 1 <= m <= 126; ldx >= m + 2,
+ * ldx % 4 == 0.  Arithmetic (k_embed, tcgen05): d - mean in fp32, both operands split into tf32 hi + lo
+ * (3 products, ~22 significant bits), fp32 tensor-core accumulation; |error| <= 1e-5 ||d - mean||.
+ * Misaligned pointers: FV_ERR_UNSUPPORTED; asynchronous on `stream`, no allocation. */
 fv_status fv_embed(const float *raw, const float *xy, const int64_t *offsets, int batch, int64_t n_total,
                    const float *img_wh, const float *pca_mean, const float *pca_basis, int m, float *X_out, int ldx,
                    fv_stream_t stream);

@@ -902,8 +902,8 @@ fv_status check_embed_args(const float *raw, const float *xy, const int64_t *off
   if (batch > 0 && (!offsets || !wh)) return fail(FV_ERR_ARG, "null offsets/img_wh");
   if (n_total > 0 && (!raw || !xy)) return fail(FV_ERR_ARG, "null raw/xy");
   if ((raw && reinterpret_cast<uintptr_t>(raw) % 16) || reinterpret_cast<uintptr_t>(mean) % 16 ||
-      (xy && reinterpret_cast<uintptr_t>(xy) % 8) || (wh && reinterpret_cast<uintptr_t>(wh) % 8))
-    return fail(FV_ERR_UNSUPPORTED, "raw/mean must be 16-byte and xy/img_wh 8-byte aligned");
+      (xy && reinterpret_cast<uintptr_t>(xy) % 16) || (wh && reinterpret_cast<uintptr_t>(wh) % 8))
+    return fail(FV_ERR_UNSUPPORTED, "raw/mean/xy must be 16-byte and img_wh 8-byte aligned (TMA)");
   return FV_OK;
 }
 
@@ -912,17 +912,61 @@ fv_status launch_embed(const float *raw, const float *xy, const int64_t *offsets
                        cudaStream_t st) {
   if (n_total == 0 || batch == 0) return FV_OK;
   EmbedParams e;
-  e.raw = raw; e.xy = xy; e.offsets = offsets; e.wh = wh; e.mean = mean; e.basis = basis; e.out = out;
-  e.n = n_total; e.batch = batch; e.m = m; e.mpad = (m + 7) / 8 * 8; e.ldx = ldx;
-  const int smem = (kEmbIn * e.mpad + kEmbRows * kEmbXStride) * 4;
-  if (cudaFuncSetAttribute(k_embed, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return cuda_check("k_embed attribute");
-  int dev = 0, sms = 148;
+  e.xy = xy; e.offsets = offsets; e.wh = wh; e.mean = mean; e.basis = basis; e.out = out;
+  e.n = n_total; e.batch = batch; e.m = m; e.ldx = ldx;
+  // raw as a 2-D tensor map: dims {128, n_total}, boxes of 32 floats x 128 rows, 128B swizzle (the tf32
+  // K-major operand layout); rows past n_total read as zero
+  CUtensorMap tmap, tmap_xy, tmap_out;
+  {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void *fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return fail(FV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)kEmbIn, (cuuint64_t)n_total};
+    cuuint64_t strides[1] = {(cuuint64_t)kEmbIn * 4};
+    cuuint32_t box[2] = {32u, 128u};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(raw), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FV_ERR_CUDA, "cuTensorMapEncodeTiled (raw) failed (%d)", (int)r);
+    // keypoints as a 1-D map of 2 n_total floats, boxes of 256 (one tile's 128 rows); past the end: zero
+    cuuint64_t dxy[1] = {(cuuint64_t)(2 * n_total)};
+    cuuint32_t bxy[1] = {256u};
+    cuuint32_t exy[1] = {1};
+    cuuint64_t sxy[1] = {(cuuint64_t)(2 * n_total) * 4};  // unused for rank 1 (the driver wants a valid array)
+    r = encode(&tmap_xy, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<float *>(xy), dxy, sxy, bxy, exy,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FV_ERR_CUDA, "cuTensorMapEncodeTiled (xy) failed (%d)", (int)r);
+    // output as {ldx, n_total}, stored in 32-dim x 32-row boxes (unswizzled, row-major staging)
+    cuuint64_t dout[2] = {(cuuint64_t)ldx, (cuuint64_t)n_total};
+    cuuint64_t sout[1] = {(cuuint64_t)ldx * 4};
+    cuuint32_t bout[2] = {32u, 32u};
+    r = encode(&tmap_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dout, sout, bout, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FV_ERR_CUDA, "cuTensorMapEncodeTiled (out) failed (%d)", (int)r);
+  }
+  static std::mutex mu;
+  static bool attr_done[64] = {};
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t ntiles = (n_total + kEmbRows - 1) / kEmbRows;
-  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * (smem <= 75 * 1024 ? 3 : 2));
-  k_embed<<<grid, 256, smem, st>>>(e);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64 || !attr_done[dev]) {
+      if (cudaFuncSetAttribute(k_embed, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmbSmemBytes) != cudaSuccess)
+        return cuda_check("k_embed attribute");
+      if (dev >= 0 && dev < 64) attr_done[dev] = true;
+    }
+  }
+  const int64_t ntiles = (n_total + 127) / 128;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count());
+  k_embed<<<grid, kEmbThreads, kEmbSmemBytes, st>>>(tmap, tmap_xy, tmap_out, e);
   g_launches += 1;
   return cuda_check("k_embed");
 }

@@ -2,9 +2,10 @@
 -> FV path (embed + encode at D = m + 2 = 82, the paper's descriptor format) against the fp64
 oracle (oracle.embed, then oracle.encode on the oracle's embedding).
 
-Tolerances: the embedding accumulates 128 fp32 products per output, so |err| <= 128 * 2^-24 * sum_k
-|b_ck (d_k - mean_k)| <= 1e-5 ||d - mean|| (Cauchy-Schwarz, orthonormal rows); the FV bound is
-north_star's 1e-4 relative L2 (the fp32 embedding moves the encoder input by ~1e-7 relative)."""
+Tolerances: k_embed (tcgen05, kind::tf32) splits both operands into tf32 hi + lo (relative
+representation error <= 2^-21 per element) and accumulates 48 UMMAs in fp32, so |err| <= (3 * 2^-21 +
+48 * 2^-23) * sum_k |b_ck (d_k - mean_k)| <= 1e-5 ||d - mean|| (Cauchy-Schwarz, orthonormal rows); the
+FV bound is north_star's 1e-4 relative L2 (the embedding moves the encoder input by ~1e-7 relative)."""
 import numpy as np
 import pytest
 import torch
@@ -41,6 +42,23 @@ def test_embed_matches_oracle(fv, m, counts):
     assert np.all(np.abs(E[:, :m] - ref[:, :m]) <= bound)
     np.testing.assert_allclose(E[:, m:m + 2], ref[:, m:], rtol=1e-7)
     assert np.all(E[:, m + 2:] == 0)
+
+
+@pytest.mark.parametrize("scale", [255.0, 1.0 / 512])
+def test_embed_any_input_scale(fv, scale):
+    """Unnormalised (0..255) and tiny SIFT values: the tf32 split keeps the fp32 exponent range, so the
+    relative bound holds at any scale (an fp16 split would overflow or go subnormal); ragged tail."""
+    m = 80
+    mean, B = fvgen.make_pca(m, seed=14)
+    gmm = fvgen.make_embedded_gmm(16, m, seed=15)
+    raw, xy, off, wh = fvgen.make_raw_frames(gmm, (mean, B), [4001, 130], seed=16)
+    raw = (raw * scale).astype(np.float32)
+    mean = (mean * scale).astype(np.float32)
+    E = fv.embed(dev(raw), dev(xy), dev(off), dev(wh), dev(mean), dev(B)).cpu().numpy()
+    ref = oracle.embed(raw, xy, off, wh, mean, B)
+    bound = 1e-5 * np.linalg.norm(raw.astype(np.float64) - mean, axis=1)[:, None] + 1e-30
+    assert np.all(np.abs(E[:, :m] - ref[:, :m]) <= bound)
+    np.testing.assert_allclose(E[:, m:m + 2], ref[:, m:], rtol=1e-7)
 
 
 @pytest.mark.parametrize("tau", [0.0, 1e-6])
