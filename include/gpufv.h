@@ -59,7 +59,8 @@ enum {
   FV_NORM_NONE = 2,           /* raw Alg.1 sums U, V                                            */
   FV_NORM_MASK = 3,
   FV_SIGMA_IS_STDDEV = 1u << 4, /* `sigmas` are standard deviations (default: variances, A1)    */
-  FV_DETERMINISTIC = 1u << 5,   /* accepted for compatibility; every path is deterministic        */
+  /* bit 5 is reserved: every path is deterministic (fixed-order reductions, no float atomics whose
+     order varies), so there is no determinism flag */
   FV_PREPARED = 1u << 6,        /* `ws` already holds this GMM prepared by fv_gmm_prepare: skip a1 */
   FV_SPARSE_STATS = 1u << 7     /* threshold > 0, D <= 64, K <= 256: accumulate only the pairs gamma > tau
                                    on the CUDA cores (Alg. 5 early termination, round-to-nearest fp32 sums)

@@ -24,7 +24,6 @@ NORM_IMPROVED = 0
 NORM_POWER_L2 = 1
 NORM_NONE = 2
 SIGMA_IS_STDDEV = 1 << 4
-DETERMINISTIC = 1 << 5
 PREPARED = 1 << 6
 SPARSE_STATS = 1 << 7  # threshold > 0: survivor (Alg. 5) accumulation instead of the dense tensor-core GEMM2
 _RAW_LOGLIK = 1 << 8

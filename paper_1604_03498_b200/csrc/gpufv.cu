@@ -203,7 +203,7 @@ fv_status check_gmm_args(int K, int D, const float *w, const float *mu, const fl
   if (K > kMaxK) return fail(FV_ERR_UNSUPPORTED, "K=%d > %d", K, kMaxK);
   if (D > kDMax) return fail(FV_ERR_UNSUPPORTED, "D=%d > %d", D, kDMax);
   if (need_d4 && D % 4 != 0) return fail(FV_ERR_UNSUPPORTED, "D=%d is not a multiple of 4 (pad, reading A13)", D);
-  const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_DETERMINISTIC | FV_PREPARED | FV_SPARSE_STATS;
+  const unsigned known = FV_NORM_MASK | FV_SIGMA_IS_STDDEV | FV_PREPARED | FV_SPARSE_STATS;
   if (flags & ~known) return fail(FV_ERR_ARG, "unknown flag bits 0x%x", flags & ~known);
   if ((flags & FV_NORM_MASK) == 3) return fail(FV_ERR_ARG, "invalid normalisation mode 3");
   return FV_OK;
@@ -258,9 +258,12 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   unsigned *counters = (unsigned *)((double *)at(ws, L.norm2) + (size_t)(batch > 0 ? batch : 1) * kFinMaxParts);
   k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles), L.ncl,
                                  (int *)at(ws, L.cstart), (int *)at(ws, L.cown), counters, rflags);
+  Stats2Params p;
+  // one set whose rows are known here: no offsets (fv_encode, the E-step), or one image of a full call
+  // (offsets = {0, n_total} by the header contract; host-pipeline chunks pass rows >= 0 and keep the table)
+  p.single_rows = (!offsets || (batch == 1 && rows < 0)) ? n_single : -1;
   if (!offsets) offsets = off1;
   g_launches += 1;
-  Stats2Params p;
   p.X = X;
   p.offsets = offsets;
   p.tile_start = (const int64_t *)at(ws, L.tiles);
@@ -418,14 +421,15 @@ fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStrea
     return cuda_check("k_finalize_img");
   }
   // a handful of narrow images straight after k_stats: 4x the blocks (k_finalize_lat)
-  const int64_t lat_grid = (int64_t)((K + kFinJ - 1) / kFinJ) * batch * kLatZ;
+  const int lat_x = (K + kLatJ - 1) / kLatJ, lat_z = (D + kLatK - 1) / kLatK;
+  const int64_t lat_grid = (int64_t)lat_x * batch * lat_z;
   if (after_stats && f.slots && f.n_cls == 0 && K <= kImgK && D <= kDP && lat_grid <= sm_count() &&
-      ((K + kFinJ - 1) / kFinJ) * kLatZ <= kFinMaxParts) {
+      lat_x * lat_z <= kFinMaxParts) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.gridDim = dim3((K + kFinJ - 1) / kFinJ, batch, kLatZ);
+    cfg.gridDim = dim3(lat_x, batch, lat_z);
     cfg.blockDim = dim3(kLatThreads, 1, 1);
     cfg.stream = st;
     cfg.attrs = attr;

@@ -280,7 +280,9 @@ struct FinParams {
 constexpr int kMaxCls = 32;     // classes of the fused linear scoring
 
 constexpr int kFinJ = 32;       // Gaussians per finalize block
-constexpr int kFinMaxParts = (kMaxK / kFinJ) * (kDMax / kDP);  // finalize blocks per image
+// partial-norm slots per image: k_finalize uses (K / 32) x (D / 64) <= 32 blocks, k_finalize_lat
+// (K / 16) x (D / 16) <= 64
+constexpr int kFinMaxParts = 64;
 constexpr int kFinKI = kDP / 8; // dims per thread: k = kq + 8 i
 
 // S0_j (gamma units) and S1_jk, S2_jk (about c, unscaled; k = kq + 8 i) of image b from the slots:
@@ -884,48 +886,134 @@ __global__ void __launch_bounds__(kImgThreads, 1) k_finalize_img(const FinParams
   }
 }
 
-// Latency path (a handful of images, K <= 256, D <= 64, slots): the tile-parallel finalize with
-// 4x the blocks — block (x, b, z) takes Gaussians 32x .. +31 and dims 8z .. +7 and 32 + 8z .. +7 with
-// 64 threads (fin_tile_seg's thread layout with kr = tid / 8 < 8) — because one image's segment
-// reads are bound by the per-SM L2 -> SM bandwidth of the few SMs that hold its blocks (a 5,000-
-// descriptor frame over 10 segments pulls 1.3 MB: ~7 us on 8 SMs).  All blocks are co-resident
-// (grid <= SMs): each publishes its partial sum of squares, waits for its image's siblings and writes
-// its sub-tile once, scaled (as k_finalize<.., kSync>).
-constexpr int kLatThreads = 64;
-constexpr int kLatZ = 4;     // dim slices per 64 dims
-constexpr int kLatSegs = 8;  // segment loads in flight per thread (the chain is L2-latency bound)
+// Latency path (a handful of images, K <= 256, D <= 64, slots).  A single frame is spread over many
+// clusters (one or a few tiles each, so k_stats finishes early), so its finalize reads many segments.
+// That reduction is bound by how many L2 requests each SM keeps in flight, not by bandwidth (a 5,000-
+// descriptor frame over 40 segments is 5 MB), so every load is a full 128-byte line: a block owns 32
+// Gaussians x 8 dims, and a warp-wide float4 load covers 4 slot rows x 128 B (8 lanes per row; rows =
+// (segment, feature) pairs).  Thread t (Gaussian group g = t % 8, row slot rs = t / 8) sums the rows
+// rs, rs + 32, ... = one feature (S1 or S2 of one dim) over every other segment, all loads of a round
+// in flight (kLatRows rows: 40 segments in one round); the two segment parities and the S0 partials
+// are combined through shared memory in a fixed order.  Grid (K/32, batch, D/8) <= the SM count (one
+// wave, every block co-resident): blocks publish their partial sum of squares, wait for their image's
+// siblings and write their (32 x 8) sub-tile once, scaled (as k_finalize<.., kSync>).
+constexpr int kLatThreads = 256;
+constexpr int kLatJ = 32, kLatK = 8;   // Gaussians x dims per block
+constexpr int kLatRows = 20;           // slot rows per thread per round of loads
 __global__ void __launch_bounds__(kLatThreads) k_finalize_lat(const FinParams p) {
   ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
   TRF(1);
-  __shared__ float sU[kFinJ][kDP + 1], sV[kFinJ][kDP + 1];
-  __shared__ double s_S0[kFinJ];
+  __shared__ double s_part[2][2 * kLatK][kLatJ];  // [segment parity][feature][Gaussian]
+  __shared__ double s_p0[kLatThreads / 8][kLatJ];  // S0 partials [row slot][Gaussian]
+  __shared__ double s_S0[kLatJ];
   __shared__ double s_red[kLatThreads / 32];
   __shared__ int s_segs[kImgMaxSeg];
   __shared__ int s_nseg;
-  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x;
-  const int j0 = blockIdx.x * kFinJ, nj = min(kFinJ, p.K - j0), kb = 8 * (int)blockIdx.z;
+  const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, lane = tid & 31;
+  const int j0 = blockIdx.x * kLatJ, k0 = blockIdx.z * kLatK;
   const bool direct = p.tile_start[p.batch] >= (int64_t)p.ncl;
+  const int clo = p.cown[2 * b], chi = p.cown[2 * b + 1];
   if (!direct && tid == 0) {  // some cluster owns no tile: scan for the image's non-empty segments
     const int ft = (int)p.tile_start[b], lt = (int)p.tile_start[b + 1];
     int ns = 0;
-    for (int c = p.cown[2 * b]; c <= p.cown[2 * b + 1] && ns < kImgMaxSeg; ++c) {
+    for (int c = clo; c <= chi && ns < kImgMaxSeg; ++c) {
       const int st = p.cstart[c], en = p.cstart[c + 1];
       if ((st > ft ? st : ft) < (en < lt ? en : lt)) s_segs[ns++] = c;
     }
     s_nseg = ns;
   }
   __syncthreads();
-  const int lo = p.cown[2 * b], hi = p.cown[2 * b + 1];
-  double ss = fin_tile_seg<kLatSegs>(p, b, j0, kb, tid, 1, kLatThreads, sU, sV, direct ? nullptr : s_segs, lo,
-                           direct ? hi - lo + 1 : s_nseg, (double)(p.offsets[b + 1] - p.offsets[b]), s_S0, j0);
+  const int nseg = direct ? chi - clo + 1 : s_nseg;
+  auto seg = [&](int i) { return direct ? clo + i : s_segs[i]; };
+  const size_t seg_stride = (size_t)2 * p.dpad * p.Kp;
+  // this thread's output (j, k) and its coefficients: independent of the segments, in flight with them
+  const int ok_ = tid & (kLatK - 1), oj = tid >> 3;  // 8 consecutive dims per 8 lanes (coalesced stores)
+  const int j = j0 + oj, k = k0 + ok_;
+  const bool valid = k < p.D && j < p.K;
+  const double N = (double)(p.offsets[b + 1] - p.offsets[b]);
+  double xs = 0.0, mup = 0.0, isd = 0.0, ivar = 0.0, psu = 0.0, psv = 0.0;
+  if (valid) {
+    xs = p.xinv[k];  // 1 / (2^14 2^e_k): powers of two, exact
+    const double *cf = p.coef + (size_t)k * p.Kp + j;
+    mup = cf[0]; isd = cf[kDMax * p.Kp]; ivar = cf[2 * kDMax * p.Kp];
+    psu = p.pscale[j]; psv = p.pscale[p.Kp + j];
+  }
+  TRF(8);
+  const int g = tid & 7, rs = tid >> 3;  // Gaussian group (4 Gaussians j0 + 4 g ..), row slot 0..31
+  {
+    // S1 / S2 rows: row r = 16 s + f (segment s, feature f = 2 (dim - k0) + {0: S1, 1: S2}); this
+    // thread: f = rs % 16, segments rs / 16 + 2 u
+    const int f = rs & 15, par = rs >> 4, kf = k0 + (f >> 1);
+    const size_t frow = (size_t)((f & 1) ? p.dpad + kf : kf) * p.Kp + j0 + 4 * g;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    if (kf < p.D) {
+      for (int s0 = par; s0 < nseg; s0 += 2 * kLatRows) {
+        float4 v[kLatRows];
+#pragma unroll
+        for (int u = 0; u < kLatRows; ++u) {
+          const int si = s0 + 2 * u;
+          v[u] = si < nseg ? __ldcs(reinterpret_cast<const float4 *>(p.slots + (size_t)seg_slot(seg(si), b) * seg_stride + frow))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kLatRows; ++u) { a[0] += (double)v[u].x; a[1] += (double)v[u].y; a[2] += (double)v[u].z; a[3] += (double)v[u].w; }
+      }
+    }
+    // S0 partials: pair v = 4 s + q (segment s, row group q); this thread: pairs rs + 32 u
+    double z[4] = {0.0, 0.0, 0.0, 0.0};
+    const int nv = 4 * nseg;
+    for (int v0 = rs; v0 < nv; v0 += 32 * 8) {
+      float4 w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = v0 + 32 * u;
+        w[u] = v < nv ? __ldcs(reinterpret_cast<const float4 *>(p.s0slots + ((size_t)seg_slot(seg(v >> 2), b) * 4 + (v & 3)) * p.Kp + j0 + 4 * g))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { z[0] += (double)w[u].x; z[1] += (double)w[u].y; z[2] += (double)w[u].z; z[3] += (double)w[u].w; }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { s_part[par][f][4 * g + e] = a[e]; s_p0[rs][4 * g + e] = z[e]; }
+  }
+  TRF(5);
+  __syncthreads();
+  if (tid < kLatJ) {  // S0 of Gaussian j0 + tid: the 32 row-slot partials in fixed order
+    double S0 = 0.0;
+    for (int r = 0; r < kLatThreads / 8; ++r) S0 += s_p0[r][tid];
+    s_S0[tid] = S0 * (1.0 / (double)kPScale);  // S0 was accumulated from P = gamma 2^14
+  }
+  __syncthreads();
+  TRF(6);
+  float u = 0.f, v = 0.f;
+  double ss = 0.0;
+  if (valid) {
+    const int fl = 2 * ok_;
+    const double S0 = s_S0[oj];
+    const double s1 = (s_part[0][fl][oj] + s_part[1][fl][oj]) * xs;
+    const double s2 = (s_part[0][fl + 1][oj] + s_part[1][fl + 1][oj]) * (xs * xs * (double)kPScale);
+    double U = (s1 - mup * S0) * isd;                                  // sum gamma (x - mu)/sd
+    double V = (s2 - 2.0 * mup * s1 + mup * mup * S0) * ivar - S0;     // sum gamma ((x-mu)^2/var - 1)
+    if (p.mode != 2) {
+      const bool zero = !(N > 0.0);
+      const double invN = zero ? 0.0 : 1.0 / N;
+      if (p.mode == 0 && !zero) { U *= invN * psu; V *= invN * psv; }
+      if (zero) U = V = 0.0;
+      ss = fabs(U) + fabs(V);  // = (signed sqrt)^2
+      u = signed_sqrt((float)U);
+      v = signed_sqrt((float)V);
+    } else {
+      u = (float)U;
+      v = (float)V;
+    }
+  }
   TRF(2);
   const int part = blockIdx.z * gridDim.x + blockIdx.x, nparts = gridDim.x * gridDim.z;
-  const bool l2 = p.mode != 2;
   float sc = 1.f;
-  if (l2) {
+  if (p.mode != 2) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-    if ((tid & 31) == 0) s_red[tid >> 5] = ss;
+    if (lane == 0) s_red[tid >> 5] = ss;
     __syncthreads();
     if (tid == 0) {
       double tot = 0.0;
@@ -939,21 +1027,19 @@ __global__ void __launch_bounds__(kLatThreads) k_finalize_lat(const FinParams p)
     }
     __syncthreads();
     TRF(3);
-    double n2 = 0.0;  // fixed-order sum of the parts: the same bits in every block
-    for (int k = 0; k < nparts; ++k) n2 += __ldcg(p.norm2 + (size_t)b * kFinMaxParts + k);
+    // fixed-order sum of the parts (the same bits in every block): lane l loads parts l, l + 32, then
+    // a fixed xor tree
+    double n2 = 0.0;
+    for (int q = lane; q < nparts; q += 32) n2 += __ldcg(p.norm2 + (size_t)b * kFinMaxParts + q);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, off);
     if (n2 > 0.0) sc = (float)(1.0 / sqrt(n2));
-  } else {
-    __syncthreads();
   }
-  // this block's (nj x 16) sub-tile: thread -> (Gaussian r, 8-dim strip half, dim)
-  const int KD = p.K * p.D;
-  float *o = p.out + (size_t)b * 2 * KD + (size_t)j0 * p.D;
-  for (int t = tid; t < nj * 16; t += kLatThreads) {
-    const int r = t >> 4, c = t & 15, k = kb + (c & 7) + 32 * (c >> 3);
-    if (k < p.D) {
-      o[(size_t)r * p.D + k] = sU[r][k - kb] * sc;
-      o[KD + (size_t)r * p.D + k] = sV[r][k - kb] * sc;
-    }
+  if (valid) {
+    const int KD = p.K * p.D;
+    float *o = p.out + (size_t)b * 2 * KD + (size_t)j * p.D + k;
+    o[0] = u * sc;
+    o[KD] = v * sc;
   }
   TRF(4);
 }

@@ -80,6 +80,7 @@ constexpr uint32_t kTZr = 0, kTL = 256, kTS = 384;
 // named barriers (0 = __syncthreads)
 constexpr uint32_t kBarLane0 = 1;  // 1..4: the 4 WORK warps of a TMEM lane group (k_stats_w's quarter combine)
 constexpr uint32_t kBarXchgLocal = 5;  // the 16 WORK warps of a single-CTA cluster (k_stats, K <= 128)
+constexpr uint32_t kBarWorkSetup = 6;  // the 16 WORK warps: bias / scale tables loaded (k_stats)
 
 struct Stats2Params {
   const float *X;             // n_total x D (also behind the tensor map; used for L2 prefetch)
@@ -96,6 +97,8 @@ struct Stats2Params {
   int kfold;                  // GEMM2 restart period in tiles (kFold, or kFoldLong for large sets)
   int *rflags;                // batch: range flags (bit 0: a row with non-finite log-likelihoods), zeroed by k_schedule
   int batch, D, K, Kp;
+  int64_t single_rows;        // >= 0: one set of this many rows whose schedule is known without k_schedule
+                              // (tile_start = {0, T}): the tile walk then reads nothing from global memory
   int ldx;                    // row stride of X in floats (>= D, % 4 == 0)
   float threshold;
   int gamma_mode;
@@ -108,6 +111,11 @@ struct TileWalker {
   const Stats2Params *p;
   int t, t1, ts_b, ts_b1, off_b, off_b1, b, seg_pos;
   __device__ void load_image() {
+    if (p->single_rows >= 0) {  // one set: image 0 holds every tile
+      b = 0; ts_b = 0; ts_b1 = (int)((p->single_rows + kTileM - 1) / kTileM);
+      off_b = 0; off_b1 = (int)p->single_rows;
+      return;
+    }
     while (t >= (int)p->tile_start[b + 1]) ++b;  // skips empty images
     ts_b = (int)p->tile_start[b]; ts_b1 = (int)p->tile_start[b + 1];
     off_b = (int)p->offsets[b]; off_b1 = (int)p->offsets[b + 1];
@@ -115,7 +123,9 @@ struct TileWalker {
   __device__ void init(const Stats2Params &pp, int t0_, int t1_) {
     p = &pp; t = t0_; t1 = t1_; b = 0; seg_pos = 0;
     ts_b = ts_b1 = off_b = off_b1 = 0;
-    if (t0_ < t1_) {
+    if (t0_ < t1_ && pp.single_rows >= 0) {
+      load_image();
+    } else if (t0_ < t1_) {
       int lo = 0, hi = pp.batch;
       while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (pp.tile_start[mid] <= t0_) lo = mid; else hi = mid - 1; }
       b = lo;
@@ -255,11 +265,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
 #ifdef GPUFV_TRACE
   if (p.trace && cid == 0 && rank == 0 && tid == 0) p.trace[7720] = ptx::globaltimer();
 #endif
-  // ---------------- setup
-  {
-    for (int i = tid; i < kG; i += kThreads2) s_bias[i] = p.bias[rank * kG + i];
-    if (tid < kDP) { s_sc[tid] = p.xscale[tid]; s_ncs[tid] = -(p.xshift[tid] * p.xscale[tid]); }
-  }
+  // ---------------- setup (the bias / feature-scale tables are loaded by the WORK warps after the
+  // cluster sync: their global-load latency stays off the CTA-wide barriers)
   if (warp == 0) { tmem_alloc(s_tmem, kTmemCols); tmem_relinquish(); }
   if (tid == 0) {
     mbar_init(&bars[B_XFULL0], 1); mbar_init(&bars[B_XFULL1], 1);
@@ -286,10 +293,12 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   cluster_sync();
   if (tid == 0) TRP(2);
   griddep_launch_dependents();  // k_finalize may start its prologue
-  griddep_wait();               // k_schedule's tile prefix sums are complete and visible
+  // k_schedule's tile prefix sums (and its zeroing of the range flags the WORK warps may set) are
+  // complete and visible.  A single set's schedule needs no table: only the WORK warps wait then.
+  if (p.single_rows < 0 || warp >= kWarpWork0) griddep_wait();
   if (tid == 0) TRP(3);
 
-  const int64_t T = p.tile_start[p.batch];
+  const int64_t T = p.single_rows >= 0 ? (p.single_rows + kTileM - 1) / kTileM : p.tile_start[p.batch];
   const int t0 = (int)((int64_t)cid * T / ncl), t1 = (int)((int64_t)(cid + 1) * T / ncl);
   const int n = t1 - t0;
 
@@ -466,6 +475,12 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       __syncwarp();  // the P(i) stores of this warp reuse the staging bytes
     };
 
+    {
+      const int wt = tid - kWarpWork0 * 32;
+      for (int i = wt; i < kG; i += kWarpsWork * 32) s_bias[i] = p.bias[rank * kG + i];
+      if (wt < kDP) { s_sc[wt] = p.xscale[wt]; s_ncs[wt] = -(p.xshift[wt] * p.xscale[wt]); }
+      named_bar_sync(kBarWorkSetup, kWarpsWork * 32);
+    }
     float s0acc[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) s0acc[j] = 0.f;
