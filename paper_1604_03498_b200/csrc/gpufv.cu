@@ -2,7 +2,7 @@
 // layout, launches.  No allocation, no synchronisation (except fv_encode_batched_host, which must
 // return host results), no CPU fallback: every step of the path runs in the kernels below.
 // Experiment knobs (environment, read once per process; defaults are the measured best):
-//   GPUFV_MIN_TILES=<n>   minimum tiles per cluster for small launches (default 3)
+//   GPUFV_MIN_TILES=<n>   minimum tiles per cluster for small launches (default 2)
 //   GPUFV_FIN_TILES=1     force the tile-parallel finalize for large batches (default: k_finalize_img)
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -66,7 +66,7 @@ int sm_count() {
 
 // Tile family: D <= 64 -> k_stats (128 Gaussians per CTA, cluster <= 4); 64 < D <= 128 -> k_stats_w
 // (64 Gaussians per CTA, cluster <= 8).  K <= 512 for both.
-constexpr int kMinTilesPerClusterDefault = 3;
+constexpr int kMinTilesPerClusterDefault = 2;
 constexpr int kMaxSegPerImage = 26;
 // GPUFV_MIN_TILES overrides it (latency experiments only); read once per process
 int min_tiles_per_cluster() {
@@ -218,6 +218,22 @@ fv_status check_device() {
   if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) { cudaGetLastError(); return fail(FV_ERR_CUDA, "cudaGetDeviceProperties failed"); }
   if (prop.major != 10 || prop.minor != 0)
     return fail(FV_ERR_UNSUPPORTED, "device %s is sm_%d%d; this library is built for sm_100a only", prop.name, prop.major, prop.minor);
+  // Every kernel of a call prefers the maximum shared-memory carveout — the one the stats kernels
+  // need (227 KB per CTA).  With the default carveout an SM that last ran a small-SMEM kernel (the
+  // finalize, the schedule) must drain and reconfigure its L1 / shared split before it can take a
+  // stats CTA: measured ~6 us between k_schedule's entry and the first k_stats CTA of a single frame.
+  {
+    const int c = cudaSharedmemCarveoutMaxShared;
+    const void *fns[] = {(const void *)k_schedule, (const void *)k_finalize_lat, (const void *)k_finalize<false, false>,
+                         (const void *)k_finalize<false, true>, (const void *)k_finalize<true, false>,
+                         (const void *)k_finalize<true, true>, (const void *)k_finalize_img<false>,
+                         (const void *)k_finalize_img<true>, (const void *)k_reduce_stats, (const void *)k_prep_shift,
+                         (const void *)k_prep_bias, (const void *)k_prep_bias_final, (const void *)k_prep_w,
+                         (const void *)k_range_flags, (const void *)k_loglik_reduce, (const void *)k_mstep};
+    for (const void *f : fns)
+      if (cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, c) != cudaSuccess)
+        return cuda_check("carveout attribute");
+  }
   if (dev >= 0 && dev < 64) ok_dev[dev] = 1;
   return FV_OK;
 }
@@ -257,7 +273,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   int64_t *off1 = (int64_t *)at(ws, L.off1);
   unsigned *counters = (unsigned *)((double *)at(ws, L.norm2) + (size_t)(batch > 0 ? batch : 1) * kFinMaxParts);
   k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles), L.ncl,
-                                 (int *)at(ws, L.cstart), (int *)at(ws, L.cown), counters, rflags);
+                                 (int *)at(ws, L.cstart), (int *)at(ws, L.cown), counters, rflags, g_trace);
   Stats2Params p;
   // one set whose rows are known here: no offsets (fv_encode, the E-step), or one image of a full call
   // (offsets = {0, n_total} by the header contract; host-pipeline chunks pass rows >= 0 and keep the table)

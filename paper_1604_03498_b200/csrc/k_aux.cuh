@@ -190,7 +190,12 @@ __device__ __forceinline__ int64_t tile_owner(int64_t t, int64_t T, int64_t ncl)
 // Also zeroes the finalize's per-image arrival counters (so no memset node separates k_stats from
 // k_finalize in the stream) and lets k_stats start its prologue early (programmatic launch).
 __global__ void k_schedule(const int64_t *offsets, int64_t *off1, int64_t n_single, int batch, int64_t *tile_start,
-                           int ncl, int *cstart, int *cown, unsigned *counters, int *rflags) {
+                           int ncl, int *cstart, int *cown, unsigned *counters, int *rflags, long long *trace) {
+#ifdef GPUFV_TRACE
+  if (trace && threadIdx.x == 0) trace[7723] = ptx::globaltimer();
+#else
+  (void)trace;
+#endif
   __shared__ int64_t s_warp[32];
   __shared__ int64_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1042,6 +1047,9 @@ __global__ void __launch_bounds__(kLatThreads) k_finalize_lat(const FinParams p)
     o[KD] = v * sc;
   }
   TRF(4);
+#ifdef GPUFV_TRACE
+  if (p.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long *>(p.trace + 7724), (unsigned long long)ptx::globaltimer());
+#endif
 }
 
 // a6 only: slots -> fp64 stats [N, S0, S1, S2] about c (reading A19).  Same grid as k_finalize.

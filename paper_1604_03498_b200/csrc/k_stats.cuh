@@ -330,10 +330,12 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
           twp.init(p, t0, t1);
           for (int k = 0; k < 4; ++k) prefetch_l2(k);
         }
-        // box 1 (dims 32..63) after box 0 of this tile was released
-        mbar_wait(&bars[B_XEMPTY0], i & 1);
+        // box 1 (dims 32..63) after box 0 of this tile was released; tile 0's box 1 goes straight into
+        // the Z buffer (unused until copy_z(0), which follows GEMM1(0) and so every box-1 conversion):
+        // the first tile then pays one HBM round trip instead of two (latency path)
+        if (i >= 1) mbar_wait(&bars[B_XEMPTY0], i & 1);
         mbar_arrive_expect_tx(&bars[B_XFULL1], kXBoxBytes);
-        tma_load_2d(sX, &tmap_x, 32, m.row0, &bars[B_XFULL1]);
+        tma_load_2d(i == 0 ? sZ : sX, &tmap_x, 32, m.row0, &bars[B_XFULL1]);
         prefetch_l2(i + 4);
       }
     }
@@ -415,8 +417,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       mbar_wait(&bars[B_XFULL0 + box], i & 1);
       const int nrows = s_meta[i & 3].nrows;
       const uint32_t ta = tmem + kTZr + 128 * (i & 1) + lane_base;
-      if (!kD64 || nrows < kTileM) zr_box<true>(xbox, row, box, h, D, row < nrows, s_sc, s_ncs, ta);
-      else zr_box<false>(xbox, row, box, h, D, true, s_sc, s_ncs, ta);
+      const uint8_t *xb = (i == 0 && box == 1) ? smem + kS2Z : xbox;  // tile 0's box 1 sits in the Z buffer
+      if (!kD64 || nrows < kTileM) zr_box<true>(xb, row, box, h, D, row < nrows, s_sc, s_ncs, ta);
+      else zr_box<false>(xb, row, box, h, D, true, s_sc, s_ncs, ta);
       if (box == 1) tmem_st_wait();
       tc_fence_before();
       __syncwarp();

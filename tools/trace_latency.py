@@ -45,8 +45,12 @@ for _ in range(5):
     assert lib.fv_encode_batched(*args(1 << 6)) == 0  # FV_PREPARED (bit 6)
 torch.cuda.synchronize()
 lib.fv_debug_trace(vp(tr.data_ptr()))
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
 assert lib.fv_encode_batched(*args(1 << 6)) == 0
+e1.record()
 torch.cuda.synchronize()
+print(f"CUDA events around the traced call: {1e3 * e0.elapsed_time(e1):.1f} us")
 t = tr.cpu().numpy()
 P = t[7680:7696]
 t0 = P[0]
@@ -61,7 +65,7 @@ work = t[1024:1024 + 64 * 4 * 16].reshape(64, 4, 16)
 for i in range(64):
     if work[i, 0, 0]:
         print(f"  tile {i}: WORK slot 0 (L ready) {work[i, 0, 0] - t0:8d}   P write done (slot 9) {work[i, 0, 9] - t0:8d}")
-G = t[7700:7723]
+G = t[7700:7725]
 g0 = G[20]
 print("global timeline (ns from k_stats CTA 0 entry, %globaltimer):")
 for k, name in [(20, "k_stats CTA 0 entry"), (21, "k_stats CTA 0 end"), (22, "k_stats last CTA end"),
@@ -71,3 +75,7 @@ for k, name in [(20, "k_stats CTA 0 entry"), (21, "k_stats CTA 0 end"), (22, "k_
                 (4, "k_finalize block 0 end")]:
     if G[k]:
         print(f"  {name:42s} {G[k] - g0:8d}")
+if G[23]:
+    print(f"  {'k_schedule entry':42s} {G[23] - g0:8d}")
+if G[24]:
+    print(f"  {'k_finalize last block end':42s} {G[24] - g0:8d}")
