@@ -297,6 +297,30 @@ def test_stats_are_additive_over_shards():
     np.testing.assert_allclose(parts, whole, rtol=1e-11, atol=1e-12)
 
 
+def test_blocked_stats_equal_stats_on_one_set():
+    """oracle.stats_blocked (the large-set goldens' writer) = stats() of the whole set: several row
+    blocks, several per-call chunks, a ragged last block; exact and tau modes."""
+    gmm = fvgen.make_gmm(16, 6, seed=31)
+    X = fvgen.make_descriptors(gmm, 5003, seed=32)
+    for tau in (0.0, 1e-6):
+        whole = oracle.stats(X, *gmm, threshold=tau)
+        blocked = oracle.stats_blocked(X, *gmm, threshold=tau, block=257, nthreads=3)
+        np.testing.assert_allclose(blocked, whole, rtol=1e-11, atol=1e-11)
+        assert blocked[0] == X.shape[0]
+
+
+def test_blocked_em_step_equals_em_step():
+    """oracle.em_step_blocked (two passes over row blocks, thread pool) = em_step() on the same set."""
+    gmm = fvgen.make_gmm(6, 5, seed=33)
+    X = fvgen.make_descriptors(gmm, 4001, seed=34)
+    init = fvgen.make_gmm(6, 5, seed=35)
+    a = oracle.em_step(X, *init)
+    b = oracle.em_step_blocked(X, *init, block=300, workers=3)
+    for x, y in zip(a[:3], b[:3]):
+        np.testing.assert_allclose(y, x, rtol=1e-10, atol=1e-12)
+    assert abs(a[3] - b[3]) <= 1e-9 * abs(a[3])
+
+
 def test_batched_equals_per_image_and_thread_invariance():
     gmm = fvgen.make_gmm(8, 4, seed=25)
     X, off = fvgen.make_batch(gmm, [10, 0, 1, 300, 5000], seed_base=26)
