@@ -323,6 +323,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         s_meta[i & 3] = m;  // released to the WORK warps by the X_FULL phase completions below
         // box 0 (dims 0..31) after box 1 of the previous tile was released
         if (i >= 1) mbar_wait(&bars[B_XEMPTY1], (i - 1) & 1);
+        // tile 0's box-0 release (phase 0 of X_EMPTY0) is not needed for a load (its box 1 went to the Z
+        // buffer); observe it here so that every phase is waited on (compute-sanitizer synccheck)
+        if (i == 1) mbar_wait(&bars[B_XEMPTY0], 0);
         mbar_arrive_expect_tx(&bars[B_XFULL0], kXBoxBytes);
         tma_load_2d(sX, &tmap_x, 0, m.row0, &bars[B_XFULL0]);
         if (i == 0) {
@@ -489,7 +492,13 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
     for (int j = 0; j < 32; ++j) s0acc[j] = 0.f;
     int prev_b = 0;
     bool prev_fold = false, chunk_seg_first = true;
-    if (n > 0) { conv_box(0, 0); conv_box(0, 1); }
+    if (n > 0) {
+      conv_box(0, 0);
+      conv_box(0, 1);
+      // tile 0's box 1 was read from the Z buffer, which copy_z(0) overwrites: the ordering through
+      // ZR_FULL -> GEMM1(0) -> G1_DONE already holds; this barrier states it in a form racecheck sees
+      named_bar_sync(kBarWorkSetup, kWarpsWork * 32);
+    }
     for (int i = 0; i < n; ++i) {
       TRW(0);
       work_wait(&bars[B_G1_DONE], i & 1);  // L(i) ready; Zr((i+1)%2) free (GEMM1(i-1) done)
