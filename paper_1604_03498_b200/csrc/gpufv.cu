@@ -90,8 +90,10 @@ int num_clusters(int C, bool wide) {
   std::lock_guard<std::mutex> lk(mu);
   if (cache[dev][wide][C] > 0) return cache[dev][wide][C];
   const int smem = wide ? kSmemWBytes : kSmem2Bytes;
-  if (cudaFuncSetAttribute(k_stats<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+  if (cudaFuncSetAttribute(k_stats<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_sp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSpBytes) != cudaSuccess ||
@@ -110,7 +112,7 @@ int num_clusters(int C, bool wide) {
   cfg.numAttrs = 1;
   int n = 0;
   const cudaError_t e = wide ? cudaOccupancyMaxActiveClusters(&n, k_stats_w<true>, &cfg)
-                             : cudaOccupancyMaxActiveClusters(&n, k_stats<true>, &cfg);
+                             : cudaOccupancyMaxActiveClusters(&n, k_stats<true, 2>, &cfg);
   if (e != cudaSuccess || n <= 0) {
     cudaGetLastError();
     int sms = 0;
@@ -349,13 +351,16 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   if (g_prof_start) cudaEventRecord(g_prof_start, st);
   cudaError_t e;
   if (sparse) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats_sp<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_sp<false>, tmap, p);
-  else if (!is_wide(K, D)) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false>, tmap, p);
+  else if (!is_wide(K, D)) {
+    if (L.C == 1) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true, 1>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false, 1>, tmap, p);
+    else e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true, 2>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false, 2>, tmap, p);
+  }
   else e = (D == kDMax) ? cudaLaunchKernelEx(&cfg, k_stats_w<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false>, tmap, p);
   if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
   g_launches += 1;
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_stats<true>);
+    cudaFuncGetAttributes(&fa, k_stats<true, 2>);
     cudaGetLastError();
     return fail(FV_ERR_CUDA,
                 "k_stats launch: %s (grid %d x %d threads, cluster %d, dyn smem %d; kernel: %d regs, max threads %d, "

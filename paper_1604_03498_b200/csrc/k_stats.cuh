@@ -241,7 +241,11 @@ __device__ __forceinline__ void work_wait(uint64_t *bar, uint32_t parity) {
 #define TRP(slot) do { } while (0)
 #endif
 
-template <bool kD64>
+// kC = cluster size (ceil(K / 128): 1 or 2) at compile time: the exchange loops and the combine over
+// the 4 kC quarter pairs unroll without predicates (~3 % of the kernel's instructions at runtime C;
+// C4 k_stats 8.62 -> 8.21 ms).  (A third parameter compiling the per-row hooks out measured 9.41 ms:
+// the register allocation of this 96-register kernel moves with any change — measure each one.)
+template <bool kD64, int kC>
 __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ CUtensorMap tmap_x, const Stats2Params p) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + kS2Tmem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t rank = cluster_ctarank(), C = cluster_nctarank();
+  const uint32_t rank = cluster_ctarank(), C = (uint32_t)kC;
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
 
   if (tid == 0) TRP(0);
@@ -580,14 +584,11 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       TRW(12);
       float M = -3.0e38f, S = 0.f;
       {
-        float2 o[kMaxC2 * 4];
+        float2 o[kC * 4];
 #pragma unroll
-        for (int e = 0; e < kMaxC2 * 4; ++e) {
-          o[e] = make_float2(-3.0e38f, 0.f);
-          if (e < (int)C * 4) { o[e] = xb[e * kTileM + row]; M = fmaxf(M, o[e].x); }
-        }
+        for (int e = 0; e < kC * 4; ++e) { o[e] = xb[e * kTileM + row]; M = fmaxf(M, o[e].x); }
 #pragma unroll
-        for (int e = 0; e < kMaxC2 * 4; ++e) S += o[e].y * ex2_approx(o[e].x - M);
+        for (int e = 0; e < kC * 4; ++e) S += o[e].y * ex2_approx(o[e].x - M);
       }
       // per-descriptor log2-likelihood (EM, NEXT-3): log2 sum_j 2^(L_ij + b_j) = M + log2 S
       if (p.loglik_out && h == 0 && rank == 0 && row < mt.nrows) p.loglik_out[mt.row0 + row] = M + log2f(S);
