@@ -300,6 +300,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 // Split two fp32 values into packed fp16 hi and lo words: v = hi + lo to ~22 significant bits.
+//   hi = fp16(v) (round to nearest), lo = fp16(v - hi) (round to nearest)
 __device__ __forceinline__ void split2_f16(float a, float b, uint32_t &hi, uint32_t &lo) {
   __half2 h = __floats2half2_rn(a, b);
   float2 hf = __half22float2(h);
