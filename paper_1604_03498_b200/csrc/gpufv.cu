@@ -17,6 +17,8 @@
 #include <mutex>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/gpufv.h"
 #include "fv_common.cuh"
 #include "k_aux.cuh"
@@ -28,6 +30,15 @@
 using namespace gpufv;
 
 namespace {
+
+// NVTX ranges around every C-ABI entry point and each host-pipeline chunk (header-only NVTX v3: a
+// no-op unless a profiler such as nsys / ncu --nvtx is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
@@ -556,6 +567,7 @@ size_t fv_workspace_bytes_host(int64_t n_total, int batch, int K, int D, unsigne
 
 fv_status fv_gmm_prepare(const float *w, const float *mu, const float *sg, int K, int D, unsigned flags, void *ws,
                          size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_gmm_prepare");
   g_launches = 0;
   if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags)) return s;
   if (fv_status s = check_device()) return s;
@@ -569,6 +581,7 @@ fv_status fv_gmm_prepare(const float *w, const float *mu, const float *sg, int K
 fv_status fv_encode_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D, const float *w,
                             const float *mu, const float *sg, int K, float thr, unsigned flags, float *out, void *ws,
                             size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_encode_batched");
   g_launches = 0;
   if (fv_status s = check_common(X, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
   if (batch > 0 && (!offsets || !out)) return fail(FV_ERR_ARG, "null offsets/out");
@@ -579,6 +592,7 @@ fv_status fv_encode_batched(const float *X, const int64_t *offsets, int batch, i
 
 fv_status fv_encode(const float *X, int64_t N, int D, const float *w, const float *mu, const float *sg, int K,
                     float thr, unsigned flags, float *out, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_encode");
   g_launches = 0;
   if (fv_status s = check_common(X, N, 1, D, K, thr, w, mu, sg, flags)) return s;
   if (!out) return fail(FV_ERR_ARG, "null out");
@@ -656,6 +670,7 @@ fv_status encode_host_impl(const float *X_host, const int64_t *offsets_host, int
   cudaEvent_t *ev = hp->ev;
   fv_status rs = FV_OK;
   for (int k = 0; k < nch && rs == FV_OK; ++k) {
+    NvtxRange chunk_range("fv host chunk");
     const int b0 = (int)((int64_t)k * batch / nch), b1 = (int)((int64_t)(k + 1) * batch / nch);
     const int64_t r0 = offsets_host[b0], r1 = offsets_host[b1];
     if (r1 > r0 && cudaMemcpyAsync(dX + r0 * D, X_host + r0 * D, (size_t)(r1 - r0) * D * 4, cudaMemcpyHostToDevice,
@@ -690,6 +705,7 @@ extern "C" {
 fv_status fv_encode_batched_host(const float *X_host, const int64_t *offsets_host, int batch, int64_t n_total, int D,
                                  const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
                                  float *out_host, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_encode_batched_host");
   g_launches = 0;
   if (fv_status s = check_common(X_host, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
   if (batch > 0 && (!offsets_host || !out_host)) return fail(FV_ERR_ARG, "null offsets/out");
@@ -710,6 +726,7 @@ fv_status fv_encode_scored_batched(const float *X, const int64_t *offsets, int b
                                    const float *w, const float *mu, const float *sg, int K, float thr, unsigned flags,
                                    const float *svm_w, const float *svm_b, int n_cls, float *scores, float *out,
                                    void *ws, size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_encode_scored_batched");
   g_launches = 0;
   if (fv_status s = check_common(X, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
   if (batch > 0 && !offsets) return fail(FV_ERR_ARG, "null offsets");
@@ -725,6 +742,7 @@ fv_status fv_encode_scored_batched_host(const float *X_host, const int64_t *offs
                                         int D, const float *w, const float *mu, const float *sg, int K, float thr,
                                         unsigned flags, const float *svm_w, const float *svm_b, int n_cls,
                                         float *scores_host, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_encode_scored_batched_host");
   g_launches = 0;
   if (fv_status s = check_common(X_host, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
   if (batch > 0 && !offsets_host) return fail(FV_ERR_ARG, "null offsets");
@@ -739,6 +757,7 @@ fv_status fv_encode_scored_batched_host(const float *X_host, const int64_t *offs
 fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, int64_t n_total, int D, const float *w,
                            const float *mu, const float *sg, int K, float thr, unsigned flags, double *stats, void *ws,
                            size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_stats_batched");
   g_launches = 0;
   if (fv_status s = check_common(X, n_total, batch, D, K, thr, w, mu, sg, flags)) return s;
   if (batch > 0 && (!offsets || !stats)) return fail(FV_ERR_ARG, "null offsets/stats");
@@ -766,6 +785,7 @@ fv_status fv_stats_batched(const float *X, const int64_t *offsets, int batch, in
 
 fv_status fv_finalize(const double *stats, int batch, int D, const float *w, const float *mu, const float *sg, int K,
                       unsigned flags, float *out, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_finalize");
   g_launches = 0;
   if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags)) return s;
   if (batch < 0) return fail(FV_ERR_ARG, "batch < 0");
@@ -786,6 +806,7 @@ fv_status fv_finalize(const double *stats, int batch, int D, const float *w, con
 
 fv_status fv_posteriors(const float *X, int64_t N, int D, const float *w, const float *mu, const float *sg, int K,
                         float thr, unsigned flags, float *gamma, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_posteriors");
   g_launches = 0;
   // bit 8 (undocumented, tests only): write raw log2-likelihoods instead of gamma
   const int mode = (flags & (1u << 8)) ? 2 : 1;
@@ -867,6 +888,7 @@ extern "C" {
 
 fv_status fv_gmm_estep(const float *X, int64_t N, int D, const float *w, const float *mu, const float *sg, int K,
                        unsigned flags, double *stats, double *loglik, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_gmm_estep");
   g_launches = 0;
   if (fv_status s = check_common(X, N, 1, D, K, 0.f, w, mu, sg, flags)) return s;
   if (!stats || !loglik) return fail(FV_ERR_ARG, "null stats/loglik");
@@ -880,6 +902,7 @@ fv_status fv_gmm_estep(const float *X, int64_t N, int D, const float *w, const f
 fv_status fv_gmm_mstep(const double *stats, int D, const float *w, const float *mu, const float *sg, int K,
                        unsigned flags, float var_floor_abs, float var_floor_rel, float prior_floor, float *w_new,
                        float *mu_new, float *var_new, void *ws, size_t ws_bytes, fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_gmm_mstep");
   g_launches = 0;
   if (fv_status s = check_gmm_args(K, D, w, mu, sg, flags)) return s;
   if (!stats || !w_new || !mu_new || !var_new) return fail(FV_ERR_ARG, "null stats/output");
@@ -896,6 +919,7 @@ fv_status fv_gmm_em_step(const float *X, int64_t N, int D, const float *w, const
                          unsigned flags, float var_floor_abs, float var_floor_rel, float prior_floor, float *w_new,
                          float *mu_new, float *var_new, double *loglik, void *ws, size_t ws_bytes,
                          fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_gmm_em_step");
   g_launches = 0;
   if (fv_status s = check_common(X, N, 1, D, K, 0.f, w, mu, sg, flags)) return s;
   if (!w_new || !mu_new || !var_new || !loglik) return fail(FV_ERR_ARG, "null output");
@@ -1003,6 +1027,7 @@ extern "C" {
 fv_status fv_embed(const float *raw, const float *xy, const int64_t *offsets, int batch, int64_t n_total,
                    const float *img_wh, const float *pca_mean, const float *pca_basis, int m, float *X_out, int ldx,
                    fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_embed");
   g_launches = 0;
   if (fv_status s = check_embed_args(raw, xy, offsets, batch, n_total, img_wh, pca_mean, pca_basis, m)) return s;
   if (n_total > 0 && !X_out) return fail(FV_ERR_ARG, "null X_out");
@@ -1026,6 +1051,7 @@ fv_status fv_embed_encode_batched(const float *raw, const float *xy, const int64
                                   const float *pca_basis, int m, const float *w, const float *mu, const float *sg,
                                   int K, float thr, unsigned flags, float *out, void *ws, size_t ws_bytes,
                                   fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_embed_encode_batched");
   g_launches = 0;
   const int D = m + 2;
   if (fv_status s = check_embed_args(raw, xy, offsets, batch, n_total, img_wh, pca_mean, pca_basis, m)) return s;
@@ -1047,6 +1073,7 @@ fv_status fv_embed_encode_batched(const float *raw, const float *xy, const int64
 
 fv_status fv_range_flags(const void *ws, size_t ws_bytes, int64_t n_total, int batch, int K, int D, int32_t *flags_out,
                          fv_stream_t stream) {
+  NvtxRange nvtx_range("fv_range_flags");
   g_launches = 0;
   if (K < 1 || D < 1 || K > kMaxK || D > kDMax || n_total < 0 || batch < 0) return fail(FV_ERR_ARG, "bad sizes");
   if (batch > 0 && !flags_out) return fail(FV_ERR_ARG, "null flags_out");
