@@ -143,6 +143,7 @@ struct Layout {
   size_t spart;                                           // fused scoring partial dots (n_cls > 0)
   size_t llrows, llparts, emstats;                        // EM: per-row log2-likelihoods, reduction, stats
   size_t emb;                                             // embedded descriptors (n_total x ldx), NEXT-2
+  size_t rflagc;                                          // per-CTA range flags (fused single-frame schedule)
   size_t hx, hoff, hout;                                  // _host entry point
   size_t total;
 };
@@ -187,6 +188,7 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   L.cown = o;     o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 8, 256);
   L.norm2 = o;    o = align_up(o + (size_t)(batch > 0 ? batch : 1) * (kFinMaxParts * 8 + 4), 1024);  // norm parts + tickets
   L.rflags = o;   o = align_up(o + (size_t)(batch > 0 ? batch : 1) * 4, 256);
+  L.rflagc = o;   o = align_up(o + (size_t)L.ncl * L.C * 4, 256);
   L.s0slots = o;  o = align_up(o + (size_t)(L.ncl + batch) * 4 * L.Kp * 4, 1024);
   L.slots = o;    o = align_up(o + (size_t)L.nslots * 2 * L.dpad * L.Kp * 4, 1024);
   L.spart = o;    o = align_up(o + (size_t)(n_cls > 0 ? batch : 0) * kFinMaxParts * n_cls * 8, 1024);
@@ -279,20 +281,30 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
 fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets, int64_t n_single, int batch, int D,
                        int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st,
                        float *loglik_rows = nullptr, int ldx = 0, int rf_base = 0, int64_t rows = -1,
-                       bool sparse_req = false) {
+                       bool sparse_req = false, bool fuse = false) {
   if (ldx <= 0) ldx = D;
   int *rflags = (int *)at(ws, L.rflags) + rf_base;
   // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
   int64_t *off1 = (int64_t *)at(ws, L.off1);
   unsigned *counters = (unsigned *)((double *)at(ws, L.norm2) + (size_t)(batch > 0 ? batch : 1) * kFinMaxParts);
-  k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles), L.ncl,
-                                 (int *)at(ws, L.cstart), (int *)at(ws, L.cown), counters, rflags, g_trace);
+  // fuse (a single frame whose finalize is k_finalize_lat): no k_schedule — k_stats writes the tables
+  if (!fuse) {
+    k_schedule<<<1, 1024, 0, st>>>(offsets, off1, n_single, batch, (int64_t *)at(ws, L.tiles), L.ncl,
+                                   (int *)at(ws, L.cstart), (int *)at(ws, L.cown), counters, rflags, g_trace);
+    g_launches += 1;
+  }
   Stats2Params p;
+  p.fused_sched = fuse ? 1 : 0;
+  p.sched_tiles = (int64_t *)at(ws, L.tiles);
+  p.sched_off1 = off1;
+  p.sched_cstart = (int *)at(ws, L.cstart);
+  p.sched_cown = (int *)at(ws, L.cown);
+  p.sched_counters = counters;
+  p.rflag_cta = (int *)at(ws, L.rflagc);
   // one set whose rows are known here: no offsets (fv_encode, the E-step), or one image of a full call
   // (offsets = {0, n_total} by the header contract; host-pipeline chunks pass rows >= 0 and keep the table)
   p.single_rows = (!offsets || (batch == 1 && rows < 0)) ? n_single : -1;
   if (!offsets) offsets = off1;
-  g_launches += 1;
   p.X = X;
   p.offsets = offsets;
   p.tile_start = (const int64_t *)at(ws, L.tiles);
@@ -358,7 +370,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   cfg.dynamicSmemBytes = is_wide(K, D) ? kSmemWBytes : sparse ? kSmemSpBytes : kSmem2Bytes;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = fuse ? 1 : 2;  // the first kernel of a fused call waits for the stream normally
   if (g_prof_start) cudaEventRecord(g_prof_start, st);
   cudaError_t e;
   if (sparse) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats_sp<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_sp<false>, tmap, p);
@@ -406,10 +418,17 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.b_base = 0;
   f.svm_w = nullptr; f.svm_b = nullptr; f.scores = nullptr; f.n_cls = 0;
   f.spart = (double *)at(ws, L.spart);
+  f.rflag_cta = nullptr; f.nflag = 0; f.rflags = nullptr;
   f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
   f.mode = (int)(flags & FV_NORM_MASK);
   f.dpad = L.dpad;
   return f;
+}
+
+// The latency finalize (k_finalize_lat) takes a launch: one wave of (K/32) x batch x (D/8) blocks.
+bool lat_finalize_fits(int K, int D, int batch) {
+  const int lat_x = (K + kLatJ - 1) / kLatJ, lat_z = (D + kLatK - 1) / kLatK;
+  return K <= kImgK && D <= kDP && (int64_t)lat_x * batch * lat_z <= sm_count() && lat_x * lat_z <= kFinMaxParts;
 }
 
 // after_stats: launched right behind k_stats (whose k_schedule zeroed the counters): programmatic
@@ -454,9 +473,7 @@ fv_status launch_finalize(const FinParams &f, int batch, int K, int D, cudaStrea
   }
   // a handful of narrow images straight after k_stats: 4x the blocks (k_finalize_lat)
   const int lat_x = (K + kLatJ - 1) / kLatJ, lat_z = (D + kLatK - 1) / kLatK;
-  const int64_t lat_grid = (int64_t)lat_x * batch * lat_z;
-  if (after_stats && f.slots && f.n_cls == 0 && K <= kImgK && D <= kDP && lat_grid <= sm_count() &&
-      lat_x * lat_z <= kFinMaxParts) {
+  if (after_stats && f.slots && f.n_cls == 0 && lat_finalize_fits(K, D, batch)) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -519,10 +536,20 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   if (!(flags & FV_PREPARED))
     if (fv_status s = launch_prep(L, w, mu, sg, K, D, flags, ws, st)) return s;
   if (batch == 0) return FV_OK;
+  // One frame whose finalize is k_finalize_lat: k_stats writes the schedule tables itself (no k_schedule
+  // launch on the latency path; GPUFV_FUSED_SCHED=0 keeps the separate kernel, for A/B runs)
+  static const bool fuse_env = [] { const char *e = std::getenv("GPUFV_FUSED_SCHED"); return !(e && e[0] == '0'); }();
+  const bool fuse = fuse_env && batch == 1 && rows < 0 && n_total > 0 && !sparse && !is_wide(K, D) && sc.n_cls == 0 &&
+                    lat_finalize_fits(K, D, batch);
   if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx, rf_base, rows,
-                                 sparse))
+                                 sparse, fuse))
     return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
+  if (fuse) {  // the finalize ORs the per-CTA range flags into the image's flag word
+    f.rflag_cta = (const int *)at(ws, L.rflagc);
+    f.nflag = L.ncl * L.C;
+    f.rflags = (int *)at(ws, L.rflags) + rf_base;
+  }
   f.out = out;
   f.svm_w = sc.w; f.svm_b = sc.b; f.n_cls = sc.n_cls; f.scores = sc.scores;
   return launch_finalize(f, batch, K, D, st);

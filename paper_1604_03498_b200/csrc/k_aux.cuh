@@ -179,8 +179,7 @@ __global__ void k_range_flags(const int *rflags, const int *gflag, int batch, in
   if (b < batch) flags_out[b] = rflags[b] | *gflag;
 }
 
-// Owner cluster of global tile t under the static split [c T / ncl, (c+1) T / ncl).
-__device__ __forceinline__ int64_t tile_owner(int64_t t, int64_t T, int64_t ncl) { return ((t + 1) * ncl - 1) / T; }
+
 
 // tile_start[0] = 0, tile_start[b+1] = sum_{b' <= b} ceil(N_b' / 128).  One block of 1024 threads.
 // offsets == nullptr means a single set of n_single rows: {0, n_single} is written to off1 and used.
@@ -273,6 +272,10 @@ struct FinParams {
   double *spart;              // batch x kFinMaxParts x n_cls: each block's partial dot products
   int n_cls;
   long long *trace;           // debug (GPUFV_TRACE builds): globaltimer points of block 0, slots 7700..
+  // fused single-frame schedule (k_finalize_lat only): per-CTA range flags of k_stats, ORed into rflags[0]
+  const int *rflag_cta;
+  int nflag;
+  int *rflags;
 };
 
 #ifdef GPUFV_TRACE
@@ -908,6 +911,11 @@ constexpr int kLatRows = 20;           // slot rows per thread per round of load
 __global__ void __launch_bounds__(kLatThreads) k_finalize_lat(const FinParams p) {
   ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
   TRF(1);
+  if (p.rflag_cta && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) {
+    int fl = 0;  // fused schedule: the image's range flag from k_stats' per-CTA words
+    for (int c = 0; c < p.nflag; ++c) fl |= p.rflag_cta[c];
+    p.rflags[0] = fl;
+  }
   __shared__ double s_part[2][2 * kLatK][kLatJ];  // [segment parity][feature][Gaussian]
   __shared__ double s_p0[kLatThreads / 8][kLatJ];  // S0 partials [row slot][Gaussian]
   __shared__ double s_S0[kLatJ];

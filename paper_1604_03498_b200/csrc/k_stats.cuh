@@ -62,6 +62,7 @@ constexpr int kS2Cs = kS2Bias + kG * 4;              // float[64]  -c_k 2^e_k
 constexpr int kS2Sc = kS2Cs + kDP * 4;               // float[64]  2^e_k
 constexpr int kS2Xchg = kS2Sc + kDP * 4;             // float2[2 parity][kMaxC2 ranks][4 quarters][128 rows] (m, s)
 constexpr int kS2Meta = kS2Xchg + 2 * kMaxC2 * 4 * kTileM * 8;  // TileMeta[4]
+constexpr int kS2Flag = kS2Meta + 124;               // int: this CTA saw a range failure (fused schedule)
 constexpr int kS2Bar = kS2Meta + 128;                // uint64 barriers
 constexpr int kNumBars = 16;
 constexpr int kS2Tmem = kS2Bar + kNumBars * 8;
@@ -99,6 +100,13 @@ struct Stats2Params {
   int batch, D, K, Kp;
   int64_t single_rows;        // >= 0: one set of this many rows whose schedule is known without k_schedule
                               // (tile_start = {0, T}): the tile walk then reads nothing from global memory
+  // fused schedule (single-frame latency path: no k_schedule launched).  CTA (0, 0) writes the tables
+  // the finalize reads and zeroes its ticket; range reports go to one flag word per CTA (written
+  // unconditionally at the end), which the finalize ORs into rflags[0] — nothing needs zeroing first.
+  int fused_sched;
+  int64_t *sched_tiles, *sched_off1;
+  int *sched_cstart, *sched_cown, *rflag_cta;
+  unsigned *sched_counters;
   int ldx;                    // row stride of X in floats (>= D, % 4 == 0)
   float threshold;
   int gamma_mode;
@@ -258,6 +266,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   float *s_sc = reinterpret_cast<float *>(smem + kS2Sc);
   float2 *s_xchg = reinterpret_cast<float2 *>(smem + kS2Xchg);
   TileMeta *s_meta = reinterpret_cast<TileMeta *>(smem + kS2Meta);
+  volatile int *s_flag = reinterpret_cast<volatile int *>(smem + kS2Flag);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kS2Bar);
   uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + kS2Tmem);
 
@@ -273,6 +282,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   // cluster sync: their global-load latency stays off the CTA-wide barriers)
   if (warp == 0) { tmem_alloc(s_tmem, kTmemCols); tmem_relinquish(); }
   if (tid == 0) {
+    *s_flag = 0;
     mbar_init(&bars[B_XFULL0], 1); mbar_init(&bars[B_XFULL1], 1);
     mbar_init(&bars[B_XEMPTY0], kWarpsWork); mbar_init(&bars[B_XEMPTY1], kWarpsWork);
     mbar_init(&bars[B_ZR_FULL], kWarpsWork);
@@ -305,6 +315,15 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   const int64_t T = p.single_rows >= 0 ? (p.single_rows + kTileM - 1) / kTileM : p.tile_start[p.batch];
   const int t0 = (int)((int64_t)cid * T / ncl), t1 = (int)((int64_t)(cid + 1) * T / ncl);
   const int n = t1 - t0;
+  if (p.fused_sched && cid == 0 && rank == 0 && warp == kWarpTma && lane == 1) {
+    // k_schedule's tables for a single set (the finalize reads them after this grid completes)
+    p.sched_tiles[0] = 0; p.sched_tiles[1] = T;
+    p.sched_off1[0] = 0; p.sched_off1[1] = p.single_rows;
+    for (int c = 0; c <= ncl; ++c) p.sched_cstart[c] = (int)((int64_t)c * T / ncl);
+    p.sched_cown[0] = T > 0 ? (int)tile_owner(0, T, ncl) : 0;
+    p.sched_cown[1] = T > 0 ? (int)tile_owner(T - 1, T, ncl) : -1;
+    p.sched_counters[0] = 0u;
+  }
 
   if (warp == kWarpTma) {
     // ======================================================= tile walk + X producer (TMA)
@@ -595,7 +614,10 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       // this quarter's gamma_ij = e_ij 2^(m_h - M) / S; P = gamma 2^14
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
       if (row >= mt.nrows) alpha_p = 0.f;
-      else if (!(S > 0.5f && S < 3.0e38f)) range_bad(p, mt.b, alpha_p, h == 0 && rank == 0);
+      else if (!(S > 0.5f && S < 3.0e38f)) {
+        if (p.fused_sched) { alpha_p = __int_as_float(0x7fffffff); *s_flag = 1; }
+        else range_bad(p, mt.b, alpha_p, h == 0 && rank == 0);
+      }
       TRW(6);
       // Zr(i+1) box 1: its TMA load started when box 0 was released above (a single 16 KB stage)
       if (i + 1 < n) conv_box(i + 1, 1);
@@ -666,6 +688,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   tc_fence_before();
   __syncthreads();
   if (tid == 0) TRP(8);
+  if (p.fused_sched && tid == 0) p.rflag_cta[cid * kC + rank] = *s_flag;
   cluster_sync();
   if (tid == 0) TRP(9);
 #ifdef GPUFV_TRACE
