@@ -105,3 +105,21 @@ def test_raw_to_fv_odd_dims(fv, m, K):
     assert np.all(out[1] == 0)
     for b in (0, 2, 3):
         assert np.linalg.norm(out[b] - ref[b]) / np.linalg.norm(ref[b]) < 1e-4
+
+
+def test_embed_many_small_images_per_tile(fv):
+    """Hundreds of 0..9-descriptor images (several images in every 128-row tile, empty ones between):
+    each row's keypoint is normalised by its own image's size (the epilogue's walk from the tile's
+    first image)."""
+    m = 30
+    mean, B = fvgen.make_pca(m, seed=17)
+    gmm = fvgen.make_embedded_gmm(8, m, seed=18)
+    rng = np.random.default_rng(19)
+    counts = [int(c) for c in rng.integers(0, 10, size=400)]
+    raw, xy, off, wh = fvgen.make_raw_frames(gmm, (mean, B), counts, seed=20)
+    wh = (wh * rng.uniform(0.5, 2.0, size=wh.shape)).astype(np.float32)  # a different size per image
+    E = fv.embed(dev(raw), dev(xy), dev(off), dev(wh), dev(mean), dev(B)).cpu().numpy()
+    ref = oracle.embed(raw, xy, off, wh, mean, B)
+    np.testing.assert_allclose(E[:, m:m + 2], ref[:, m:], rtol=1e-7)
+    bound = 1e-5 * np.linalg.norm(raw.astype(np.float64) - mean, axis=1)[:, None] + 1e-30
+    assert np.all(np.abs(E[:, :m] - ref[:, :m]) <= bound)

@@ -320,3 +320,40 @@ def test_c4_stream_full_size_sampled(fv):
     for f in (0, 1, 55, 56, 2048, 4095):
         ref = oracle.encode(X[f * P:(f + 1) * P], *gmm_np, threshold=TAU)
         assert rel_l2(out[f], ref) <= FV_RTOL
+
+
+_FUSED_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import fvgen, paper_1604_03498_b200 as fv
+gmm_np = fvgen.make_gmm(256, 64, seed=1604)
+g = fv.GMM(*gmm_np)
+outs = []
+for n, seed in ((5000, 901), (129, 902), (17714, 903)):
+    X = torch.from_numpy(fvgen.make_descriptors(gmm_np, n, seed=seed)).cuda()
+    outs.append(fv.encode(X, g, threshold=1e-6).cpu().numpy())
+    off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
+    outs.append(fv.encode_batched(X, off, g, threshold=0.0).cpu().numpy()[0])
+np.save(sys.argv[2], np.stack([o.ravel() for o in outs]))
+"""
+
+
+def test_fused_schedule_equals_separate_schedule(fv, tmp_path):
+    """Single-frame calls run without k_schedule (k_stats writes the finalize's tables, per-CTA range
+    flags): the FVs are bitwise those of the path with the separate schedule kernel (GPUFV_FUSED_SCHED=0,
+    read once per process, hence subprocesses) — fv_encode and one-image fv_encode_batched, one tile, a
+    ragged tile and the paper's 17,714-descriptor geometry."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        path = str(tmp_path / f"fused{flag}.npy")
+        r = subprocess.run([sys.executable, "-c", _FUSED_SCRIPT, root, path],
+                           env=dict(os.environ, GPUFV_FUSED_SCHED=flag), capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[flag] = np.load(path)
+    assert np.array_equal(res["0"], res["1"])
+    assert np.all(np.isfinite(res["1"]))
