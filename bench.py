@@ -1097,7 +1097,14 @@ def main():
                      "kernel": "k_stats", "kernel_ms": kms, "kernel_share_of_step": kms / ms_per_step,
                      "flop_per_desc": FLOP_PER_DESC,
                      "issued_tensor_frac": achieved * ISSUED_FLOP_PER_DESC / FLOP_PER_DESC / peak_tf,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     # achieved HBM of the same kernel (ncu DRAM bytes per launch / live kernel
+                     # time) against the measured copy bandwidth: the kernel is not HBM-bound
+                     "hbm": (None if not traffic else {
+                         "achieved_gbs": traffic / (kms * 1e-3) / 1e9,
+                         "peak_gbs": float(load_peaks().get("hbm_gbs", 7700.0)),
+                         "frac": traffic / (kms * 1e-3) / 1e9 / float(load_peaks().get("hbm_gbs", 7700.0)),
+                         "compulsory_bytes_per_desc": D * 4})},
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
