@@ -174,3 +174,23 @@ def test_binding_rejects_host_offsets(fv):
         fv.stats_batched(X, torch.tensor([0, 10]), gmm)
     with pytest.raises(ValueError):
         fv.encode_scored_batched(X, torch.tensor([0, 10]), gmm, torch.zeros(1, 2 * 16 * 8, device="cuda"))
+
+
+@pytest.mark.parametrize("K", [256, 100])
+def test_single_frame_fused_schedule_reports_range(fv, K):
+    """A single frame takes the fused schedule (no k_schedule: per-CTA flag words ORed by the finalize).
+    An outlier row makes the frame NaN and flagged; the next call on the same workspace with clean data
+    clears the flag (the words are written unconditionally, nothing relies on prior zeroing)."""
+    gmm_np = fvgen.make_gmm(K, 64, seed=43)
+    X, off = fvgen.make_batch(gmm_np, [5000], seed_base=44)
+    rms, c = rms_and_c(gmm_np)
+    bad = X.copy()
+    bad[4321, 7] = np.float32(c[7] + 2000 * rms[7])
+    gmm = fv.GMM(*gmm_np)
+    ws = fv.Workspace()
+    out = fv.encode(dev(bad), gmm, threshold=1e-6, ws=ws).cpu().numpy()
+    assert np.all(np.isnan(out))
+    assert list(fv.range_flags(ws, 5000, 1, gmm).cpu().numpy()) == [1]
+    out = fv.encode(dev(X), gmm, threshold=1e-6, ws=ws).cpu().numpy()
+    assert list(fv.range_flags(ws, 5000, 1, gmm).cpu().numpy()) == [0]
+    assert rel_l2(out, oracle.encode(X, *gmm_np, threshold=1e-6)) <= FV_RTOL
