@@ -143,7 +143,7 @@ struct Layout {
   size_t spart;                                           // fused scoring partial dots (n_cls > 0)
   size_t llrows, llparts, emstats;                        // EM: per-row log2-likelihoods, reduction, stats
   size_t emb;                                             // embedded descriptors (n_total x ldx), NEXT-2
-  size_t rflagc;                                          // per-CTA range flags (fused single-frame schedule)
+  size_t rflagc;                                          // per-CTA range words (fused single-frame schedule)
   size_t hx, hoff, hout;                                  // _host entry point
   size_t total;
 };
@@ -294,13 +294,7 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
     g_launches += 1;
   }
   Stats2Params p;
-  p.fused_sched = fuse ? 1 : 0;
-  p.sched_tiles = (int64_t *)at(ws, L.tiles);
-  p.sched_off1 = off1;
-  p.sched_cstart = (int *)at(ws, L.cstart);
-  p.sched_cown = (int *)at(ws, L.cown);
   p.sched_counters = counters;
-  p.rflag_cta = (int *)at(ws, L.rflagc);
   // one set whose rows are known here: no offsets (fv_encode, the E-step), or one image of a full call
   // (offsets = {0, n_total} by the header contract; host-pipeline chunks pass rows >= 0 and keep the table)
   p.single_rows = (!offsets || (batch == 1 && rows < 0)) ? n_single : -1;
@@ -317,7 +311,8 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.gamma_out = gamma;
   p.loglik_out = loglik_rows;
   p.trace = g_trace;
-  p.rflags = rflags;
+  p.rflags = fuse ? (int *)at(ws, L.rflagc) : rflags;  // fused: one range word per CTA (see Stats2Params)
+  p.rflag_cta = fuse ? 1 : 0;
   if (rows < 0) rows = n_single;  // rows of this launch's images (n_total unless a host-pipeline chunk)
   p.kfold = (batch > 0 && rows / batch >= kLongSetRows) ? kFoldLong : kFold;
   p.batch = batch;
@@ -418,7 +413,7 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.b_base = 0;
   f.svm_w = nullptr; f.svm_b = nullptr; f.scores = nullptr; f.n_cls = 0;
   f.spart = (double *)at(ws, L.spart);
-  f.rflag_cta = nullptr; f.nflag = 0; f.rflags = nullptr;
+  f.rflag_cta = nullptr; f.nflag = 0; f.rflags = nullptr; f.fused_n = -1;
   f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
   f.mode = (int)(flags & FV_NORM_MASK);
   f.dpad = L.dpad;
@@ -539,16 +534,19 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   // One frame whose finalize is k_finalize_lat: k_stats writes the schedule tables itself (no k_schedule
   // launch on the latency path; GPUFV_FUSED_SCHED=0 keeps the separate kernel, for A/B runs)
   static const bool fuse_env = [] { const char *e = std::getenv("GPUFV_FUSED_SCHED"); return !(e && e[0] == '0'); }();
+  // (every cluster must own a tile: the finalize takes clusters 0 .. ncl-1 as the set's segments)
   const bool fuse = fuse_env && batch == 1 && rows < 0 && n_total > 0 && !sparse && !is_wide(K, D) && sc.n_cls == 0 &&
-                    lat_finalize_fits(K, D, batch);
+                    lat_finalize_fits(K, D, batch) && (int64_t)L.ncl <= (n_total + kTileM - 1) / kTileM;
   if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx, rf_base, rows,
                                  sparse, fuse))
     return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
-  if (fuse) {  // the finalize ORs the per-CTA range flags into the image's flag word
+  if (fuse) {  // the finalize ORs the per-CTA range flags into the image's flag word and derives the
+               // single set's segments (every cluster owns >= 1 of its T >= ncl tiles) and N itself
     f.rflag_cta = (const int *)at(ws, L.rflagc);
     f.nflag = L.ncl * L.C;
     f.rflags = (int *)at(ws, L.rflags) + rf_base;
+    f.fused_n = n_total;
   }
   f.out = out;
   f.svm_w = sc.w; f.svm_b = sc.b; f.n_cls = sc.n_cls; f.scores = sc.scores;

@@ -272,10 +272,11 @@ struct FinParams {
   double *spart;              // batch x kFinMaxParts x n_cls: each block's partial dot products
   int n_cls;
   long long *trace;           // debug (GPUFV_TRACE builds): globaltimer points of block 0, slots 7700..
-  // fused single-frame schedule (k_finalize_lat only): per-CTA range flags of k_stats, ORed into rflags[0]
+  // fused single-frame schedule (k_finalize_lat only): k_stats' per-CTA range words, ORed into rflags[0]
   const int *rflag_cta;
   int nflag;
   int *rflags;
+  int64_t fused_n;            // >= 0: fused single set of fused_n rows (segments = clusters 0 .. ncl-1, N = fused_n)
 };
 
 #ifdef GPUFV_TRACE
@@ -924,8 +925,9 @@ __global__ void __launch_bounds__(kLatThreads) k_finalize_lat(const FinParams p)
   __shared__ int s_nseg;
   const int b = p.b_base + (int)blockIdx.y, tid = threadIdx.x, lane = tid & 31;
   const int j0 = blockIdx.x * kLatJ, k0 = blockIdx.z * kLatK;
-  const bool direct = p.tile_start[p.batch] >= (int64_t)p.ncl;
-  const int clo = p.cown[2 * b], chi = p.cown[2 * b + 1];
+  const bool fused = p.fused_n >= 0;  // no k_schedule ran: a single set over every cluster
+  const bool direct = fused || p.tile_start[p.batch] >= (int64_t)p.ncl;
+  const int clo = fused ? 0 : p.cown[2 * b], chi = fused ? p.ncl - 1 : p.cown[2 * b + 1];
   if (!direct && tid == 0) {  // some cluster owns no tile: scan for the image's non-empty segments
     const int ft = (int)p.tile_start[b], lt = (int)p.tile_start[b + 1];
     int ns = 0;
@@ -943,7 +945,7 @@ __global__ void __launch_bounds__(kLatThreads) k_finalize_lat(const FinParams p)
   const int ok_ = tid & (kLatK - 1), oj = tid >> 3;  // 8 consecutive dims per 8 lanes (coalesced stores)
   const int j = j0 + oj, k = k0 + ok_;
   const bool valid = k < p.D && j < p.K;
-  const double N = (double)(p.offsets[b + 1] - p.offsets[b]);
+  const double N = fused ? (double)p.fused_n : (double)(p.offsets[b + 1] - p.offsets[b]);
   double xs = 0.0, mup = 0.0, isd = 0.0, ivar = 0.0, psu = 0.0, psv = 0.0;
   if (valid) {
     xs = p.xinv[k];  // 1 / (2^14 2^e_k): powers of two, exact

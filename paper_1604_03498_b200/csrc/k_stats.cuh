@@ -49,6 +49,7 @@ constexpr int kMaxC2 = 2;                        // K <= 256 in this kernel (lar
 // per-tile metadata published by the TMA thread (ring of 4: slot t % 4 stays valid well past tile t)
 struct TileMeta {
   int row0, nrows, b, t, flags;  // flags: 1 seg_last, 2 chunk_first, 4 fold, 8 seg_first
+  int rb;                        // range-report word: b, or this CTA's own word (fused schedule)
 };
 
 // shared memory map (offsets from a 1024-aligned base)
@@ -62,7 +63,6 @@ constexpr int kS2Cs = kS2Bias + kG * 4;              // float[64]  -c_k 2^e_k
 constexpr int kS2Sc = kS2Cs + kDP * 4;               // float[64]  2^e_k
 constexpr int kS2Xchg = kS2Sc + kDP * 4;             // float2[2 parity][kMaxC2 ranks][4 quarters][128 rows] (m, s)
 constexpr int kS2Meta = kS2Xchg + 2 * kMaxC2 * 4 * kTileM * 8;  // TileMeta[4]
-constexpr int kS2Flag = kS2Meta + 124;               // int: this CTA saw a range failure (fused schedule)
 constexpr int kS2Bar = kS2Meta + 128;                // uint64 barriers
 constexpr int kNumBars = 16;
 constexpr int kS2Tmem = kS2Bar + kNumBars * 8;
@@ -100,12 +100,14 @@ struct Stats2Params {
   int batch, D, K, Kp;
   int64_t single_rows;        // >= 0: one set of this many rows whose schedule is known without k_schedule
                               // (tile_start = {0, T}): the tile walk then reads nothing from global memory
-  // fused schedule (single-frame latency path: no k_schedule launched).  CTA (0, 0) writes the tables
-  // the finalize reads and zeroes its ticket; range reports go to one flag word per CTA (written
-  // unconditionally at the end), which the finalize ORs into rflags[0] — nothing needs zeroing first.
-  int fused_sched;
-  int64_t *sched_tiles, *sched_off1;
-  int *sched_cstart, *sched_cown, *rflag_cta;
+  // Range reports go to rflags[meta.rb]: rb = b with k_schedule (which zeroes the flags).  The fused
+  // single-frame schedule (no k_schedule launched; the finalize derives the set's segments itself)
+  // gives every CTA its own word (rflag_cta = 1: rb = b + CTA index, zeroed by the CTA at its start)
+  // and the finalize ORs them into the image's flag — no word has to be zeroed before the kernel.
+  // CTA (0, 0) zeroes the finalize's ticket.  The index is computed by the tile walker (TMA thread),
+  // not in the WORK loop: writing the schedule tables here, or computing the word in the loop, grew
+  // k_stats' spill area (-17 % / -2 % on the throughput path).
+  int rflag_cta;
   unsigned *sched_counters;
   int ldx;                    // row stride of X in floats (>= D, % 4 == 0)
   float threshold;
@@ -117,7 +119,7 @@ struct Stats2Params {
 // next image.  32-bit state: the host guarantees n_total < 2^30.
 struct TileWalker {
   const Stats2Params *p;
-  int t, t1, ts_b, ts_b1, off_b, off_b1, b, seg_pos;
+  int t, t1, ts_b, ts_b1, off_b, off_b1, b, seg_pos, rb_off;
   __device__ void load_image() {
     if (p->single_rows >= 0) {  // one set: image 0 holds every tile
       b = 0; ts_b = 0; ts_b1 = (int)((p->single_rows + kTileM - 1) / kTileM);
@@ -128,8 +130,8 @@ struct TileWalker {
     ts_b = (int)p->tile_start[b]; ts_b1 = (int)p->tile_start[b + 1];
     off_b = (int)p->offsets[b]; off_b1 = (int)p->offsets[b + 1];
   }
-  __device__ void init(const Stats2Params &pp, int t0_, int t1_) {
-    p = &pp; t = t0_; t1 = t1_; b = 0; seg_pos = 0;
+  __device__ void init(const Stats2Params &pp, int t0_, int t1_, int cta = 0) {
+    p = &pp; t = t0_; t1 = t1_; b = 0; seg_pos = 0; rb_off = pp.rflag_cta ? cta : 0;
     ts_b = ts_b1 = off_b = off_b1 = 0;
     if (t0_ < t1_ && pp.single_rows >= 0) {
       load_image();
@@ -144,6 +146,7 @@ struct TileWalker {
     TileMeta m;
     m.t = t;
     m.b = b;
+    m.rb = b + rb_off;
     m.row0 = off_b + (t - ts_b) * kTileM;
     const int rem = off_b1 - m.row0;
     m.nrows = rem < kTileM ? rem : kTileM;
@@ -266,7 +269,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   float *s_sc = reinterpret_cast<float *>(smem + kS2Sc);
   float2 *s_xchg = reinterpret_cast<float2 *>(smem + kS2Xchg);
   TileMeta *s_meta = reinterpret_cast<TileMeta *>(smem + kS2Meta);
-  volatile int *s_flag = reinterpret_cast<volatile int *>(smem + kS2Flag);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kS2Bar);
   uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + kS2Tmem);
 
@@ -282,7 +284,10 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   // cluster sync: their global-load latency stays off the CTA-wide barriers)
   if (warp == 0) { tmem_alloc(s_tmem, kTmemCols); tmem_relinquish(); }
   if (tid == 0) {
-    *s_flag = 0;
+    if (p.rflag_cta) {  // fused schedule: this CTA's range word; CTA (0, 0) zeroes the finalize's ticket
+      p.rflags[cid * kC + rank] = 0;
+      if (cid == 0 && rank == 0) *p.sched_counters = 0u;
+    }
     mbar_init(&bars[B_XFULL0], 1); mbar_init(&bars[B_XFULL1], 1);
     mbar_init(&bars[B_XEMPTY0], kWarpsWork); mbar_init(&bars[B_XEMPTY1], kWarpsWork);
     mbar_init(&bars[B_ZR_FULL], kWarpsWork);
@@ -315,15 +320,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   const int64_t T = p.single_rows >= 0 ? (p.single_rows + kTileM - 1) / kTileM : p.tile_start[p.batch];
   const int t0 = (int)((int64_t)cid * T / ncl), t1 = (int)((int64_t)(cid + 1) * T / ncl);
   const int n = t1 - t0;
-  if (p.fused_sched && cid == 0 && rank == 0 && warp == kWarpTma && lane == 1) {
-    // k_schedule's tables for a single set (the finalize reads them after this grid completes)
-    p.sched_tiles[0] = 0; p.sched_tiles[1] = T;
-    p.sched_off1[0] = 0; p.sched_off1[1] = p.single_rows;
-    for (int c = 0; c <= ncl; ++c) p.sched_cstart[c] = (int)((int64_t)c * T / ncl);
-    p.sched_cown[0] = T > 0 ? (int)tile_owner(0, T, ncl) : 0;
-    p.sched_cown[1] = T > 0 ? (int)tile_owner(T - 1, T, ncl) : -1;
-    p.sched_counters[0] = 0u;
-  }
 
   if (warp == kWarpTma) {
     // ======================================================= tile walk + X producer (TMA)
@@ -614,10 +610,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       // this quarter's gamma_ij = e_ij 2^(m_h - M) / S; P = gamma 2^14
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
       if (row >= mt.nrows) alpha_p = 0.f;
-      else if (!(S > 0.5f && S < 3.0e38f)) {
-        if (p.fused_sched) { alpha_p = __int_as_float(0x7fffffff); *s_flag = 1; }
-        else range_bad(p, mt.b, alpha_p, h == 0 && rank == 0);
-      }
+      else if (!(S > 0.5f && S < 3.0e38f)) range_bad(p, mt.rb, alpha_p, h == 0 && rank == 0);
       TRW(6);
       // Zr(i+1) box 1: its TMA load started when box 0 was released above (a single 16 KB stage)
       if (i + 1 < n) conv_box(i + 1, 1);
@@ -688,7 +681,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   tc_fence_before();
   __syncthreads();
   if (tid == 0) TRP(8);
-  if (p.fused_sched && tid == 0) p.rflag_cta[cid * kC + rank] = *s_flag;
   cluster_sync();
   if (tid == 0) TRP(9);
 #ifdef GPUFV_TRACE
