@@ -105,8 +105,12 @@ int num_clusters(int C, bool wide) {
       cudaFuncSetAttribute(k_stats<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_sp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSpBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_sp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSpBytes) != cudaSuccess)
     return -1;
@@ -122,7 +126,7 @@ int num_clusters(int C, bool wide) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  const cudaError_t e = wide ? cudaOccupancyMaxActiveClusters(&n, k_stats_w<true>, &cfg)
+  const cudaError_t e = wide ? cudaOccupancyMaxActiveClusters(&n, k_stats_w<true, 0>, &cfg)
                              : cudaOccupancyMaxActiveClusters(&n, k_stats<true, 2>, &cfg);
   if (e != cudaSuccess || n <= 0) {
     cudaGetLastError();
@@ -373,7 +377,12 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
     if (L.C == 1) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true, 1>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false, 1>, tmap, p);
     else e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true, 2>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false, 2>, tmap, p);
   }
-  else e = (D == kDMax) ? cudaLaunchKernelEx(&cfg, k_stats_w<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false>, tmap, p);
+  else {
+    const bool full = D == kDMax;
+    if (L.C == 8) e = full ? cudaLaunchKernelEx(&cfg, k_stats_w<true, 8>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false, 8>, tmap, p);
+    else if (L.C == 4) e = full ? cudaLaunchKernelEx(&cfg, k_stats_w<true, 4>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false, 4>, tmap, p);
+    else e = full ? cudaLaunchKernelEx(&cfg, k_stats_w<true, 0>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false, 0>, tmap, p);
+  }
   if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
   g_launches += 1;
   if (e != cudaSuccess) {

@@ -54,7 +54,9 @@ enum : int {
 // tensor-memory columns: Zr (half hf at 128 hf), L (64), S'_hf (64 each)
 constexpr uint32_t kWTZr = 0, kWTL = 256, kWTS = 320;
 
-template <bool kD128>
+// kCW = cluster size at compile time (4: K = 256 e.g. the D = 82 raw -> FV path, 8: K = 512, C5), or 0
+// for any other size (read from %cluster_nctarank): the exchange loops unroll without predicates.
+template <bool kD128, int kCW>
 __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant__ CUtensorMap tmap_x, const Stats2Params p) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
   uint32_t *s_tmem = reinterpret_cast<uint32_t *>(smem + kWTmem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t rank = cluster_ctarank(), C = cluster_nctarank();
+  const uint32_t rank = cluster_ctarank(), C = kCW > 0 ? (uint32_t)kCW : cluster_nctarank();
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
 
   // ---------------- setup
