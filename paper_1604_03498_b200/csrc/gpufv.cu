@@ -105,12 +105,18 @@ int num_clusters(int C, bool wide) {
       cudaFuncSetAttribute(k_stats<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats_w<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats_w<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats_w<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats_w<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats_w<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
-      cudaFuncSetAttribute(k_stats_w<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<true, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_sp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSpBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_sp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSpBytes) != cudaSuccess)
     return -1;
@@ -126,7 +132,7 @@ int num_clusters(int C, bool wide) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  const cudaError_t e = wide ? cudaOccupancyMaxActiveClusters(&n, k_stats_w<true, 0>, &cfg)
+  const cudaError_t e = wide ? cudaOccupancyMaxActiveClusters(&n, k_stats_w<true, 0, false>, &cfg)
                              : cudaOccupancyMaxActiveClusters(&n, k_stats<true, 2>, &cfg);
   if (e != cudaSuccess || n <= 0) {
     cudaGetLastError();
@@ -378,10 +384,15 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
     else e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true, 2>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false, 2>, tmap, p);
   }
   else {
-    const bool full = D == kDMax;
-    if (L.C == 8) e = full ? cudaLaunchKernelEx(&cfg, k_stats_w<true, 8>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false, 8>, tmap, p);
-    else if (L.C == 4) e = full ? cudaLaunchKernelEx(&cfg, k_stats_w<true, 4>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false, 4>, tmap, p);
-    else e = full ? cudaLaunchKernelEx(&cfg, k_stats_w<true, 0>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_w<false, 0>, tmap, p);
+    // instantiations: full-D fast path x cluster size (4, 8, runtime) x per-row hooks
+    using KW = void (*)(const CUtensorMap, const Stats2Params);
+    const KW kw[2][3][2] = {
+        {{k_stats_w<false, 0, false>, k_stats_w<false, 0, true>}, {k_stats_w<false, 4, false>, k_stats_w<false, 4, true>},
+         {k_stats_w<false, 8, false>, k_stats_w<false, 8, true>}},
+        {{k_stats_w<true, 0, false>, k_stats_w<true, 0, true>}, {k_stats_w<true, 4, false>, k_stats_w<true, 4, true>},
+         {k_stats_w<true, 8, false>, k_stats_w<true, 8, true>}}};
+    const bool hooks = gamma != nullptr || loglik_rows != nullptr;
+    e = cudaLaunchKernelEx(&cfg, kw[D == kDMax][L.C == 8 ? 2 : L.C == 4 ? 1 : 0][hooks], tmap, p);
   }
   if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
   g_launches += 1;

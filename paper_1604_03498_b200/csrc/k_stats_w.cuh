@@ -56,7 +56,9 @@ constexpr uint32_t kWTZr = 0, kWTL = 256, kWTS = 320;
 
 // kCW = cluster size at compile time (4: K = 256 e.g. the D = 82 raw -> FV path, 8: K = 512, C5), or 0
 // for any other size (read from %cluster_nctarank): the exchange loops unroll without predicates.
-template <bool kD128, int kCW>
+// kHooks: the per-row posterior / log-likelihood outputs (fv_posteriors, the EM E-step) are compiled
+// in; the encode instantiations leave them out (+2.5 % C5, +1 % raw -> FV at D = 82, same-box A/B).
+template <bool kD128, int kCW, bool kHooks>
 __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant__ CUtensorMap tmap_x, const Stats2Params p) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         v[j] = x0.x; v[j + 1] = x0.y; v[j + 2] = x1.x; v[j + 3] = x1.y;
         m = fmaxf(m, fmaxf(fmaxf(x0.x, x0.y), fmaxf(x1.x, x1.y)));
       }
-      if (p.gamma_mode == 2 && row < mt.nrows) {
+      if (kHooks && p.gamma_mode == 2 && row < mt.nrows) {
         float *go = p.gamma_out + (size_t)(mt.row0 + row) * p.K;
 #pragma unroll
         for (int j = 0; j < 16; ++j) { int gj = rank * kGW + 16 * h + j; if (gj < p.K) go[gj] = v[j]; }
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         S = Sg;
       }
       // per-descriptor log2-likelihood (EM, NEXT-3)
-      if (p.loglik_out && h == 0 && rank == 0 && row < mt.nrows) p.loglik_out[mt.row0 + row] = M + log2f(S);
+      if (kHooks && p.loglik_out && h == 0 && rank == 0 && row < mt.nrows) p.loglik_out[mt.row0 + row] = M + log2f(S);
       float alpha_p = __fdividef(ex2_approx(m - M), S) * kPScale;
       if (row >= mt.nrows) alpha_p = 0.f;
       else if (!(S > 0.5f && S < 3.0e38f)) range_bad(p, mt.b, alpha_p, h == 0 && rank == 0);
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         sts128(sP + off, hi[0], hi[1], hi[2], hi[3]);
         sts128(sP + kPBytesW + off, lo[0], lo[1], lo[2], lo[3]);
       }
-      if (p.gamma_mode == 1 && row < mt.nrows) {
+      if (kHooks && p.gamma_mode == 1 && row < mt.nrows) {
         float *go = p.gamma_out + (size_t)(mt.row0 + row) * p.K;
 #pragma unroll
         for (int j = 0; j < 16; ++j) { int gj = rank * kGW + 16 * h + j; if (gj < p.K) go[gj] = v[j] * (1.f / kPScale); }
