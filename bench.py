@@ -207,8 +207,17 @@ class ClockSampler:
         rows = [r for r in self.rows if self.t0 is None or (self.t0 <= r[0] <= (self.t1 or r[0]))]
         if not rows:  # timed region shorter than one sample period: use the nearest samples
             rows = self.rows[-3:]
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        if not rows:  # the sampler saw nothing (NVML hiccup): one nvidia-smi query right after the region
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=20).stdout.strip().split(",")
+                v = [c.strip() for c in out]
+                reasons = [self.NAMES[i] for i in range(4) if v[4 + i].lower() in ("active", "1", "yes")]
+                return {"sm_mhz": float(v[0]), "sm_max_mhz": float(v[1]), "reasons": reasons, "samples": 1,
+                        "source": "nvidia-smi, right after the timed region"}
+            except Exception:  # noqa: BLE001
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[3][i]})
         return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
                 "reasons": reasons, "samples": len(rows), "source": self.source}
