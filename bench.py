@@ -77,6 +77,25 @@ def self_launch(args):
     return subprocess.call(cmd)
 
 
+def rank_device(local):
+    """This rank's GPU and process-group backend.  GPUFV_BENCH_SHARE_GPU=1 is a harness test for a box
+    with one GPU: every rank runs on GPU 0 and the collectives go over gloo (NCCL refuses two ranks on
+    one device) — the N > 1 code paths run, the numbers mean nothing."""
+    import torch
+    share = os.environ.get("GPUFV_BENCH_SHARE_GPU") == "1"
+    dev = torch.device("cuda", 0 if share else local)
+    torch.cuda.set_device(dev)
+    return dev, ("gloo" if share else "nccl")
+
+
+def init_dist(dev, backend):
+    import torch.distributed as dist
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -442,11 +461,10 @@ def run_c5(args, rank, world, local):
     rank draws its shard from its own seeded stream (fvgen recipe; the set's shape and distribution are
     those of C5, its exact values depend on the world size)."""
     import torch
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev, backend = rank_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev, backend)
     import paper_1604_03498_b200 as fv
     from paper_1604_03498_b200 import dist as fvdist
     cfg = fvgen.CONFIGS["C5"]
@@ -602,11 +620,10 @@ def run_em(args, rank, world, local):
     from a different seeded GMM.  Multi-GPU: descriptor-sharded, one all_reduce of the 1+K(2D+1)+1 fp64
     values per iteration (dist.em_step_sharded), weak scaling."""
     import torch
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev, backend = rank_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev, backend)
     import paper_1604_03498_b200 as fv
     from paper_1604_03498_b200 import dist as fvdist
     n_frames = 256 * 4  # 1024 blocks of 5000 = 5.12 M rows
@@ -727,11 +744,10 @@ def run_embed(args, rank, world, local):
     plus normalised xy (D = 82, the paper's format), K = 256, tau = 1e-6; one step = fv_embed_encode_batched
     (k_embed + the encode path).  The embedding kernel is also timed alone (fp32 FMA bound)."""
     import torch
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev, backend = rank_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev, backend)
     import paper_1604_03498_b200 as fv
     m, Ke = 80, 256
     frames = min(args.frames, 1024)
@@ -848,11 +864,10 @@ def main():
         run_embed(args, rank, world, local)
         return
     import torch
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev, backend = rank_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev, backend)
     import paper_1604_03498_b200 as fv
     from paper_1604_03498_b200 import dist as fvdist
 

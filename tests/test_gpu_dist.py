@@ -59,3 +59,24 @@ def test_sharded_em_cuda_path_matches_oracle(results):
     for res in results:
         assert res["em_pi"] <= 1e-7 and res["em_mu_over_sd"] <= 1e-4
         assert res["em_var_rel"] <= 1e-4 and res["em_ll_per_desc"] <= 2e-5
+
+
+def test_bench_two_ranks_sharing_one_gpu(tmp_path):
+    """The N > 1 bench harness end to end on a one-GPU box: `bench.py --gpus 2` launches two ranks
+    itself (torch.distributed.run on 127.0.0.1); GPUFV_BENCH_SHARE_GPU=1 puts both on GPU 0 with gloo
+    collectives (NCCL refuses two ranks on one device).  Frame sharding, the self-checks, the max-over-
+    ranks timing and the single JSON line of rank 0 all run; the numbers mean nothing here."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GPUFV_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--frames", "256", "--steps", "3",
+                        "--warmup", "3", "--e2e-steps", "0", "--cpu-seconds", "0", "--no-latency", "--no-legs",
+                        "--score-steps", "0"], env=env, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] == 3
