@@ -324,7 +324,8 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   p.rflags = fuse ? (int *)at(ws, L.rflagc) : rflags;  // fused: one range word per CTA (see Stats2Params)
   p.rflag_cta = fuse ? 1 : 0;
   if (rows < 0) rows = n_single;  // rows of this launch's images (n_total unless a host-pipeline chunk)
-  p.kfold = (batch > 0 && rows / batch >= kLongSetRows) ? kFoldLong : kFold;
+  p.kfold = (batch > 0 && rows / batch >= kLongSetRows) ? kFoldLong
+            : (kFoldShort > 0 && batch > 0 && rows / batch <= kShortSetRows) ? kFoldShort : kFold;
   p.batch = batch;
   p.D = D;
   p.K = K;
