@@ -79,6 +79,7 @@ int sm_count() {
 // (64 Gaussians per CTA, cluster <= 8).  K <= 512 for both.
 constexpr int kMinTilesPerClusterDefault = 2;
 constexpr int kMaxSegPerImage = 26;
+constexpr int kMaxSegPerImageNarrow = 80;  // >= every cluster of a narrow launch: no cap
 // GPUFV_MIN_TILES overrides it (latency experiments only); read once per process
 int min_tiles_per_cluster() {
   static const int v = [] {
@@ -170,13 +171,16 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   const int64_t tmax = n_total / kTileM + batch;
   const int mt = min_tiles_per_cluster();
   if (tmax > 0) L.ncl = (int)std::min<int64_t>(L.ncl, std::max<int64_t>(1, (tmax + mt - 1) / mt));
-  // ... and at most ~kMaxSegPerImage segments per image on average: the finalize of one image costs
-  // ~1 us per extra segment (measured: one 40,000-descriptor image 157 us over 74 clusters, 92 us
-  // over 26), so a single large image uses fewer, longer cluster ranges
-  // (only for small images — up to 32 tiles per cluster at the cap; a large single set such as an EM
-  // pass or a descriptor shard needs every cluster)
-  if (batch > 0 && tmax <= (int64_t)kMaxSegPerImage * 32 * batch)
-    L.ncl = (int)std::min<int64_t>(L.ncl, (int64_t)kMaxSegPerImage * batch);
+  // ... and at most ~kMaxSegPerImage segments per image on average: the tile-parallel finalize of one
+  // image costs ~1 us per extra segment (measured: one 40,000-descriptor image 157 us over 74 clusters,
+  // 92 us over 26), so a single large image uses fewer, longer cluster ranges (only for small images —
+  // up to 32 tiles per cluster at the cap; a large single set such as an EM pass or a descriptor shard
+  // needs every cluster).  The narrow family's one-round latency finalize reads up to 40 segments per
+  // load round, so there the cap is lifted (round 2: 17,714 descriptors 42.3 -> 34.1 us, 40,000 64.7 ->
+  // 45.5 us).  A function of (n_total, batch, K, D) only, so every workspace query agrees.
+  const int seg_cap = is_wide(K, D) ? kMaxSegPerImage : kMaxSegPerImageNarrow;
+  if (batch > 0 && tmax <= (int64_t)seg_cap * 32 * batch)
+    L.ncl = (int)std::min<int64_t>(L.ncl, (int64_t)seg_cap * batch);
   // one slot per (cluster, image) segment, index cid + b (seg_slot, fv_common.cuh)
   L.n_total = n_total;
   L.nslots = (int64_t)L.ncl + batch + 1;
