@@ -140,10 +140,12 @@ def self_check_fvs(out, label):
 
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled every 20 ms (NVML; nvidia-smi -lms 100 as fallback) from
-    before the warm-up to the end of the timed region; summary() keeps the samples taken between
-    mark_start() and mark_stop() (the timed region)."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    """SM clocks and throttle reasons sampled every 20 ms from before the warm-up to the end of the timed
+    region; summary() keeps the samples taken between mark_start() and mark_stop() (the timed region).
+    Primary source: an `nvidia-smi -lms 20` subprocess whose lines carry their own timestamps (a Python
+    sampling thread can be starved of the GIL while the host thread feeds the GPU: round 2 saw 0-1
+    NVML samples in 0.18 s timed regions); NVML in a thread when nvidia-smi is missing."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -154,6 +156,18 @@ class ClockSampler:
         self.source = None
 
     def __enter__(self):
+        try:
+            target = self.bus if self.bus else str(self.index)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", target, f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi -lms 20"
+            self.t = threading.Thread(target=self._smi_loop, daemon=True)
+            self.t.start()
+            time.sleep(0.3)  # the first samples arrive before the warm-up starts
+            return self
+        except OSError:
+            self.proc = None
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -168,18 +182,8 @@ class ClockSampler:
             self.nvml, self.h, self.source = pynvml, h, "nvml"
             self.t = threading.Thread(target=self._nvml_loop, daemon=True)
             self.t.start()
-            return self
-        except Exception:  # noqa: BLE001  (no NVML: fall back to nvidia-smi)
+        except Exception:  # noqa: BLE001
             pass
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.source = "nvidia-smi"
-            self.t = threading.Thread(target=self._smi_loop, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
         return self
 
     def _nvml_loop(self):
@@ -191,27 +195,30 @@ class ClockSampler:
             try:
                 sm = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
                 r = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.rows.append((time.perf_counter(), float(sm), float(mx), [bool(r & b) for b in bits]))
+                self.rows.append((time.time(), float(sm), float(mx), [bool(r & b) for b in bits]))
             except Exception:  # noqa: BLE001
                 pass
             time.sleep(0.02)
 
     def _smi_loop(self):
+        import datetime
         for line in self.proc.stdout:
             r = [c.strip() for c in line.split(",")]
             try:
-                self.rows.append((time.perf_counter(), float(r[0]), float(r[1]),
-                                  [len(r) > 4 + i and r[4 + i] == "Active" for i in range(4)]))
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                self.rows.append((ts, float(r[1]), float(r[2]),
+                                  [len(r) > 5 + i and r[5 + i] == "Active" for i in range(4)]))
             except (ValueError, IndexError):
                 pass
 
     def mark_start(self):
-        self.t0 = time.perf_counter()
+        self.t0 = time.time()
 
     def mark_stop(self):
-        self.t1 = time.perf_counter()
+        self.t1 = time.time()
 
     def __exit__(self, *a):
+        time.sleep(0.1)  # the samples of the region's last 20 ms
         self.stop.set()
         if self.proc:
             self.proc.terminate()
@@ -221,22 +228,15 @@ class ClockSampler:
                 self.proc.kill()
         if getattr(self, "t", None):
             self.t.join(timeout=2)
+        return False
 
     def summary(self):
         rows = [r for r in self.rows if self.t0 is None or (self.t0 <= r[0] <= (self.t1 or r[0]))]
-        if not rows:  # timed region shorter than one sample period: use the nearest samples
-            rows = self.rows[-3:]
-        if not rows:  # the sampler saw nothing (NVML hiccup): one nvidia-smi query right after the region
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=20).stdout.strip().split(",")
-                v = [c.strip() for c in out]
-                reasons = [self.NAMES[i] for i in range(4) if v[4 + i].lower() in ("active", "1", "yes")]
-                return {"sm_mhz": float(v[0]), "sm_max_mhz": float(v[1]), "reasons": reasons, "samples": 1,
-                        "source": "nvidia-smi, right after the timed region"}
-            except Exception:  # noqa: BLE001
-                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        if not rows:  # timed region shorter than one sample period: the samples around it
+            near = sorted(self.rows, key=lambda r: abs(r[0] - (self.t0 or 0)))[:3]
+            rows = near
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[3][i]})
         return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
                 "reasons": reasons, "samples": len(rows), "source": self.source}
