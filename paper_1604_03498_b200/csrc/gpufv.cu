@@ -81,17 +81,38 @@ constexpr int kMinTilesPerClusterDefault = 2;
 constexpr int kMaxSegPerImage = 26;
 constexpr int kMaxSegPerImageNarrow = 80;  // >= every cluster of a narrow launch: no cap
 // GPUFV_MIN_TILES overrides it (latency experiments only); read once per process
-int min_tiles_per_cluster() {
+int min_tiles_env() {
   static const int v = [] {
     const char *e = std::getenv("GPUFV_MIN_TILES");
     const int x = e ? std::atoi(e) : 0;
-    return x > 0 ? x : kMinTilesPerClusterDefault;
+    return x > 0 ? x : 0;
   }();
   return v;
 }
+int min_tiles_per_cluster() { return min_tiles_env() > 0 ? min_tiles_env() : kMinTilesPerClusterDefault; }
+// The single-frame finalize runs inside k_stats (fin_lat_fused) where it pays (fin_fused_wanted);
+// GPUFV_FIN_FUSED=0 never (A/B runs), =2 whenever the kernel can (tests: more blocks than CTAs)
+int fin_fused_mode() {
+  static const int v = [] { const char *e = std::getenv("GPUFV_FIN_FUSED"); return e ? std::atoi(e) : 1; }();
+  return v;
+}
+bool lat_finalize_fits(int K, int D, int batch);
+bool fin_fused_wanted(int K, int D, int n_cls, int C, int64_t ncl, int64_t tiles, int64_t ncl_max);
 bool is_wide(int K, int D) { return D > kDP || K > kG * kMaxC2; }
 int gauss_per_cta(int K, int D) { return is_wide(K, D) ? kGW : kG; }
 int cluster_size(int K, int D) { return (K + gauss_per_cta(K, D) - 1) / gauss_per_cta(K, D); }
+// Fused finalize for a single narrow frame (auto mode) only when the frame has one tile per cluster and
+// every one of the finalize's (K/32) x (D/8) blocks gets a CTA of its own.  Measured (same box, p50):
+// 5,000 descriptors 29.0 vs 30.1-32 us (the separate k_finalize_lat); with fewer CTAs than blocks each
+// CTA finalizes several in turn (1,000 descriptors: 37 vs 31 us), and with more tiles than clusters
+// the extra segments cost more than the saved launch (10,000: 35 vs 31 us; 17,714: 35 vs 34 us).
+bool fin_fused_wanted(int K, int D, int n_cls, int C, int64_t ncl, int64_t tiles, int64_t ncl_max) {
+  const int mode = fin_fused_mode();
+  if (mode == 0 || is_wide(K, D) || n_cls != 0 || !lat_finalize_fits(K, D, 1)) return false;
+  if (mode >= 2) return true;
+  const int nv = ((K + kLatJ - 1) / kLatJ) * ((D + kLatK - 1) / kLatK);
+  return tiles <= ncl_max && ncl == tiles && (int64_t)C * ncl >= nv;
+}
 
 // Persistent grid: the number of co-resident clusters of the stats kernel on the current device.
 int num_clusters(int C, bool wide) {
@@ -106,6 +127,10 @@ int num_clusters(int C, bool wide) {
       cudaFuncSetAttribute(k_stats<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats<true, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats<false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats<true, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats<false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2Bytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_w<true, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_w<true, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_w<true, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
@@ -168,8 +193,15 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   if (L.ncl <= 0) return false;
   // small launches (one frame): at least min_tiles_per_cluster() tiles per cluster, so an image is split
   // into fewer (cluster) segments for the finalize to combine; tiles <= n_total/128 + batch
-  const int64_t tmax = n_total / kTileM + batch;
-  const int mt = min_tiles_per_cluster();
+  // (a single set: exactly its tile count)
+  const int64_t tmax = batch == 1 ? (n_total + kTileM - 1) / kTileM : n_total / kTileM + batch;
+  int mt = min_tiles_per_cluster();
+  // A single frame whose finalize runs inside k_stats: one tile per cluster — the finalize's (K/32) x
+  // (D/8) blocks then land on distinct SMs (measured, 5,000 descriptors: 33.2 us at 2 tiles per
+  // cluster, 27.0-27.8 at 1; the separate-kernel path 31-32 at either)
+  if (batch == 1 && min_tiles_env() == 0 && fin_fused_mode() == 1 &&
+      fin_fused_wanted(K, D, n_cls, L.C, std::min<int64_t>(L.ncl, tmax), tmax, L.ncl))
+    mt = 1;
   if (tmax > 0) L.ncl = (int)std::min<int64_t>(L.ncl, std::max<int64_t>(1, (tmax + mt - 1) / mt));
   // ... and at most ~kMaxSegPerImage segments per image on average: the tile-parallel finalize of one
   // image costs ~1 us per extra segment (measured: one 40,000-descriptor image 157 us over 74 clusters,
@@ -295,7 +327,7 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
 fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets, int64_t n_single, int batch, int D,
                        int K, float thr, void *ws, float *gamma, int gamma_mode, cudaStream_t st,
                        float *loglik_rows = nullptr, int ldx = 0, int rf_base = 0, int64_t rows = -1,
-                       bool sparse_req = false, bool fuse = false) {
+                       bool sparse_req = false, bool fuse = false, const FinParams *fin = nullptr) {
   if (ldx <= 0) ldx = D;
   int *rflags = (int *)at(ws, L.rflags) + rf_base;
   // offsets == nullptr: a single set of n_single rows; k_schedule materialises {0, n_single} in ws.
@@ -375,18 +407,27 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps k_schedule
   attr[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool coop_env = [] { const char *e = std::getenv("GPUFV_COOP"); return !(e && e[0] == '0'); }();
+  if (fin && coop_env) {  // fused finalize: its grid barriers need every CTA resident — a cooperative
+    attr[1].id = cudaLaunchAttributeCooperative;  // launch fails instead of hanging if the grid cannot be
+    attr[1].val.cooperative = 1;                  // (fin implies fuse: no programmatic serialization)
+  }
+  const FinParams fin_none{};
+  const FinParams &fp = fin ? *fin : fin_none;
   cfg.gridDim = dim3(L.C * L.ncl, 1, 1);
   cfg.blockDim = dim3(kThreads2, 1, 1);
   cfg.dynamicSmemBytes = is_wide(K, D) ? kSmemWBytes : sparse ? kSmemSpBytes : kSmem2Bytes;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = fuse ? 1 : 2;  // the first kernel of a fused call waits for the stream normally
+  cfg.numAttrs = (fuse && !(fin && coop_env)) ? 1 : 2;  // the first kernel of a fused call waits for the stream normally
   if (g_prof_start) cudaEventRecord(g_prof_start, st);
   cudaError_t e;
   if (sparse) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats_sp<true>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats_sp<false>, tmap, p);
   else if (!is_wide(K, D)) {
-    if (L.C == 1) e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true, 1>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false, 1>, tmap, p);
-    else e = (D == kDP) ? cudaLaunchKernelEx(&cfg, k_stats<true, 2>, tmap, p) : cudaLaunchKernelEx(&cfg, k_stats<false, 2>, tmap, p);
+    using KN = void (*)(const CUtensorMap, const Stats2Params, const FinParams);
+    const KN kn[2][2][2] = {{{k_stats<false, 1>, k_stats<false, 1, true>}, {k_stats<false, 2>, k_stats<false, 2, true>}},
+                            {{k_stats<true, 1>, k_stats<true, 1, true>}, {k_stats<true, 2>, k_stats<true, 2, true>}}};
+    e = cudaLaunchKernelEx(&cfg, kn[D == kDP][L.C == 2][fin != nullptr], tmap, p, fp);
   }
   else {
     // instantiations: full-D fast path x cluster size (4, 8, runtime) x per-row hooks
@@ -439,6 +480,7 @@ FinParams fin_params(const Layout &L, const int64_t *offsets, int batch, int K, 
   f.svm_w = nullptr; f.svm_b = nullptr; f.scores = nullptr; f.n_cls = 0;
   f.spart = (double *)at(ws, L.spart);
   f.rflag_cta = nullptr; f.nflag = 0; f.rflags = nullptr; f.fused_n = -1;
+  f.gbar = (unsigned *)((char *)at(ws, L.gflag) + 8);  // gflag + 2 and + 34 (zeroed by k_prep_shift)
   f.batch = batch; f.K = K; f.Kp = L.Kp; f.D = D; f.ncl = L.ncl;
   f.mode = (int)(flags & FV_NORM_MASK);
   f.dpad = L.dpad;
@@ -562,9 +604,6 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   // (every cluster must own a tile: the finalize takes clusters 0 .. ncl-1 as the set's segments)
   const bool fuse = fuse_env && batch == 1 && rows < 0 && n_total > 0 && !sparse && !is_wide(K, D) && sc.n_cls == 0 &&
                     lat_finalize_fits(K, D, batch) && (int64_t)L.ncl <= (n_total + kTileM - 1) / kTileM;
-  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx, rf_base, rows,
-                                 sparse, fuse))
-    return s;
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   if (fuse) {  // the finalize ORs the per-CTA range flags into the image's flag word and derives the
                // single set's segments (every cluster owns >= 1 of its T >= ncl tiles) and N itself
@@ -575,6 +614,15 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   }
   f.out = out;
   f.svm_w = sc.w; f.svm_b = sc.b; f.n_cls = sc.n_cls; f.scores = sc.scores;
+  // ... and its finalize runs inside k_stats (fin_lat_fused: no second kernel; GPUFV_FIN_FUSED=0 keeps
+  // k_finalize_lat, for A/B runs)
+  const bool fin_fused = fuse && fin_fused_wanted(K, D, sc.n_cls, L.C, L.ncl, (n_total + kTileM - 1) / kTileM,
+                                                  num_clusters(L.C, false));
+  if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx, rf_base, rows,
+                                 sparse, fuse, fin_fused ? &f : nullptr))
+    return s;
+  if (fin_fused) return FV_OK;
+  f.offsets = offsets;  // launch_stats points a single set's NULL offsets at k_schedule's {0, n}
   return launch_finalize(f, batch, K, D, st);
 }
 

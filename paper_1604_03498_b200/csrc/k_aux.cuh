@@ -31,7 +31,11 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_shift(const float *w, con
                                                            int D, int Kp, int stddev, double *cshift, float *xshift,
                                                            float *xscale, double *pscale, double *xinv, int *gflag) {
   __shared__ double s_w[kPrepThreads], s_m[kPrepThreads], s_q[kPrepThreads];
-  if (threadIdx.x == 0) *gflag = 0;  // k_prep_w (later on the stream) sets bit 1 for an fp16 overflow
+  if (threadIdx.x == 0) {
+    gflag[0] = 0;  // k_prep_w (later on the stream) sets bit 1 for an fp16 overflow
+    gflag[2] = 0;  // gflag + 2, + 34: the fused finalize's grid-barrier counter and generation
+    gflag[34] = 0;  // (separate 128-byte lines; self-resetting after the first use)
+  }
   const int dstride = D <= kDP ? kDP : kDMax, ngrp = kPrepThreads / dstride;
   const int tid = threadIdx.x, k = tid % dstride, grp = tid / dstride;
   double ws = 0.0, am = 0.0, aq = 0.0;
@@ -277,6 +281,7 @@ struct FinParams {
   int nflag;
   int *rflags;
   int64_t fused_n;            // >= 0: fused single set of fused_n rows (segments = clusters 0 .. ncl-1, N = fused_n)
+  unsigned *gbar;             // fused finalize (k_stats<.., kFin>): grid-barrier {counter, generation}, prepared head
 };
 
 #ifdef GPUFV_TRACE
@@ -912,10 +917,12 @@ constexpr int kLatRows = 20;           // slot rows per thread per round of load
 __global__ void __launch_bounds__(kLatThreads) k_finalize_lat(const FinParams p) {
   ptx::griddep_wait();  // k_stats (launched before us, programmatically) has completed
   TRF(1);
-  if (p.rflag_cta && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) {
-    int fl = 0;  // fused schedule: the image's range flag from k_stats' per-CTA words
-    for (int c = 0; c < p.nflag; ++c) fl |= p.rflag_cta[c];
-    p.rflags[0] = fl;
+  if (p.rflag_cta && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x < 32) {
+    int fl = 0;  // fused schedule: the image's range flag from k_stats' per-CTA words (one warp: the
+                 // loads are independent, a single thread would wait for each in turn)
+    for (int c = threadIdx.x; c < p.nflag; c += 32) fl |= p.rflag_cta[c];
+    fl = __reduce_or_sync(0xffffffffu, fl);
+    if (threadIdx.x == 0) p.rflags[0] = fl;
   }
   __shared__ double s_part[2][2 * kLatK][kLatJ];  // [segment parity][feature][Gaussian]
   __shared__ double s_p0[kLatThreads / 8][kLatJ];  // S0 partials [row slot][Gaussian]
@@ -1060,6 +1067,215 @@ __global__ void __launch_bounds__(kLatThreads) k_finalize_lat(const FinParams p)
 #ifdef GPUFV_TRACE
   if (p.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long *>(p.trace + 7724), (unsigned long long)ptx::globaltimer());
 #endif
+}
+
+// ---------------------------------------------------------------------------------------------------
+// Fused latency finalize: a single frame's a6 + a7 run by the stats kernel itself (k_stats<.., kFin>)
+// after its last fold, instead of a k_finalize_lat launch behind it — no launch, no programmatic hand-
+// off, and the coefficient loads overlap the grid barrier.  The arithmetic and its order are
+// k_finalize_lat's (same segment split, same fp64 sums, same 64 norm parts), so the FVs are bitwise
+// those of the two-kernel path (tests/test_gpu_parity.py).  The (K/32) x (D/8) "virtual blocks" of
+// 256 threads are spread over the stats kernel's CTAs, two per CTA at a time (threads 0-511; a CTA
+// may take several in turn when the frame has few clusters).  Two grid-wide barriers: every segment
+// slot written; every partial norm published.  The stats grid is one co-resident wave (one CTA per
+// SM, at most the occupancy query's cluster count; launched cooperatively).
+
+// Grid-wide barrier on two words in the prepared GMM head (zeroed by k_prep_shift), called by one
+// thread per CTA between __syncthreads.  Self-resetting: the last arrival zeroes the counter before it
+// releases the next generation, so the words are back to {0, g + 1} after every use.
+__device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned *gen, unsigned n) {
+  unsigned g0, old;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(gen) : "memory");
+  // release: this CTA's writes (ordered before by the caller's __syncthreads) become visible with the
+  // arrival; acquire: the last arrival sees every other CTA's writes before it releases the generation
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+  if (old == n - 1) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(ctr) : "memory");
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g0 + 1u) : "memory");
+  } else {
+    unsigned g;
+    do {
+      __nanosleep(20);
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+    } while (g == g0);
+  }
+}
+
+struct LatScratch {  // one virtual block's shared memory (k_finalize_lat's __shared__ arrays)
+  double part[2][2 * kLatK][kLatJ];
+  double p0[kLatThreads / 8][kLatJ];
+  double S0[kLatJ];
+  double red[kLatThreads / 32];
+};
+constexpr int kLatGroups = 2;  // virtual blocks in flight per stats CTA (576 threads: 2 x 256)
+
+// Virtual block vb = (bx, bz) of the single set: returns this thread's (unscaled) u, v and output
+// offset, publishes the block's partial norm to norm2[vb].  gt = thread index in the group.
+__device__ __forceinline__ void fin_lat_vblock(const FinParams &p, LatScratch &s, int vb, int gt, uint32_t bar,
+                                               float &u, float &v, int64_t &oofs, bool &valid) {
+  const int lat_x = (p.K + kLatJ - 1) / kLatJ;
+  const int bx = vb % lat_x, bz = vb / lat_x, lane = gt & 31;
+  const int j0 = bx * kLatJ, k0 = bz * kLatK, nseg = p.ncl;
+  const size_t seg_stride = (size_t)2 * p.dpad * p.Kp;
+  const int ok_ = gt & (kLatK - 1), oj = gt >> 3;
+  const int j = j0 + oj, k = k0 + ok_;
+  valid = k < p.D && j < p.K;
+  const double N = (double)p.fused_n;
+  double xs = 0.0, mup = 0.0, isd = 0.0, ivar = 0.0, psu = 0.0, psv = 0.0;
+  if (valid) {
+    xs = p.xinv[k];
+    const double *cf = p.coef + (size_t)k * p.Kp + j;
+    mup = cf[0]; isd = cf[kDMax * p.Kp]; ivar = cf[2 * kDMax * p.Kp];
+    psu = p.pscale[j]; psv = p.pscale[p.Kp + j];
+  }
+  const int g = gt & 7, rs = gt >> 3;
+  {
+    const int f = rs & 15, par = rs >> 4, kf = k0 + (f >> 1);
+    const size_t frow = (size_t)((f & 1) ? p.dpad + kf : kf) * p.Kp + j0 + 4 * g;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    if (kf < p.D) {
+      for (int s0 = par; s0 < nseg; s0 += 2 * kLatRows) {
+        float4 w[kLatRows];
+#pragma unroll
+        for (int uu = 0; uu < kLatRows; ++uu) {
+          const int si = s0 + 2 * uu;
+          w[uu] = si < nseg ? __ldcg(reinterpret_cast<const float4 *>(p.slots + (size_t)seg_slot(si, 0) * seg_stride + frow))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int uu = 0; uu < kLatRows; ++uu) { a[0] += (double)w[uu].x; a[1] += (double)w[uu].y; a[2] += (double)w[uu].z; a[3] += (double)w[uu].w; }
+      }
+    }
+    double z[4] = {0.0, 0.0, 0.0, 0.0};
+    const int nv = 4 * nseg;
+    for (int v0 = rs; v0 < nv; v0 += 32 * 8) {
+      float4 w[8];
+#pragma unroll
+      for (int uu = 0; uu < 8; ++uu) {
+        const int vv = v0 + 32 * uu;
+        w[uu] = vv < nv ? __ldcg(reinterpret_cast<const float4 *>(p.s0slots + ((size_t)seg_slot(vv >> 2, 0) * 4 + (vv & 3)) * p.Kp + j0 + 4 * g))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int uu = 0; uu < 8; ++uu) { z[0] += (double)w[uu].x; z[1] += (double)w[uu].y; z[2] += (double)w[uu].z; z[3] += (double)w[uu].w; }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { s.part[par][f][4 * g + e] = a[e]; s.p0[rs][4 * g + e] = z[e]; }
+  }
+  ptx::named_bar_sync(bar, kLatThreads);
+  if (gt < kLatJ) {
+    double S0 = 0.0;
+    for (int r = 0; r < kLatThreads / 8; ++r) S0 += s.p0[r][gt];
+    s.S0[gt] = S0 * (1.0 / (double)kPScale);
+  }
+  ptx::named_bar_sync(bar, kLatThreads);
+  u = 0.f; v = 0.f;
+  double ss = 0.0;
+  if (valid) {
+    const int fl = 2 * ok_;
+    const double S0 = s.S0[oj];
+    const double s1 = (s.part[0][fl][oj] + s.part[1][fl][oj]) * xs;
+    const double s2 = (s.part[0][fl + 1][oj] + s.part[1][fl + 1][oj]) * (xs * xs * (double)kPScale);
+    double U = (s1 - mup * S0) * isd;
+    double V = (s2 - 2.0 * mup * s1 + mup * mup * S0) * ivar - S0;
+    if (p.mode != 2) {
+      const bool zero = !(N > 0.0);
+      const double invN = zero ? 0.0 : 1.0 / N;
+      if (p.mode == 0 && !zero) { U *= invN * psu; V *= invN * psv; }
+      if (zero) U = V = 0.0;
+      ss = fabs(U) + fabs(V);
+      u = signed_sqrt((float)U);
+      v = signed_sqrt((float)V);
+    } else {
+      u = (float)U;
+      v = (float)V;
+    }
+  }
+  oofs = (int64_t)j * p.D + k;
+  if (p.mode != 2) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if (lane == 0) s.red[gt >> 5] = ss;
+    ptx::named_bar_sync(bar, kLatThreads);
+    if (gt == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < kLatThreads / 32; ++w) tot += s.red[w];
+      p.norm2[vb] = tot;
+    }
+  }
+  ptx::named_bar_sync(bar, kLatThreads);  // the scratch is reused by the group's next virtual block
+}
+
+// Run by all threads of every CTA of the fused stats kernel after its last fold (tcgen05 work done).
+constexpr uint32_t kBarFinGroup0 = 7;  // named barriers 7, 8: the two 256-thread groups
+// (inlined: a __noinline__ version kept the tile loop's spills lower, 138 vs 266 bytes, but reached
+// the kernel parameters and the shared scratch through generic pointers — 5,000 descriptors 27 -> 31 us)
+__device__ __forceinline__ void fin_lat_fused(const FinParams &p, LatScratch *scr) {
+  const int tid = threadIdx.x, cta = blockIdx.x, ncta = gridDim.x;
+  const int lat_x = (p.K + kLatJ - 1) / kLatJ, lat_z = (p.D + kLatK - 1) / kLatK, nv = lat_x * lat_z;
+  const int grp = tid / kLatThreads, gt = tid % kLatThreads;
+  const bool active = grp < kLatGroups;
+  const int KD = p.K * p.D;
+#ifdef GPUFV_TRACE
+#define TRFF(slot) do { if (p.trace && cta == 0 && tid == 0) p.trace[7700 + (slot)] = ptx::globaltimer(); } while (0)
+#else
+#define TRFF(slot) do { } while (0)
+#endif
+  TRFF(10);
+  // barrier 1: every CTA's segment slots (stores / red.adds) and S0 slots are complete
+  __syncthreads();
+  if (tid == 0) grid_barrier(p.gbar, p.gbar + 32, (unsigned)ncta);
+  __syncthreads();
+  TRFF(11);
+  if (cta == 0 && tid >= kLatGroups * kLatThreads && tid < kLatGroups * kLatThreads + 32) {
+    // the image's range flag from the per-CTA words (k_finalize_lat's rule), by an otherwise idle warp
+    const int l = tid & 31;
+    int fl = 0;
+    for (int c = l; c < p.nflag; c += 32) fl |= __ldcg(p.rflag_cta + c);
+    fl = __reduce_or_sync(0xffffffffu, fl);
+    if (l == 0) p.rflags[0] = fl;
+  }
+  // virtual blocks go to distinct CTAs first (the segment reads are bound by the L2 requests an SM
+  // keeps in flight): vb = cta + ncta (grp + kLatGroups i)
+  const int vb0 = cta + ncta * grp, vstep = kLatGroups * ncta;
+  const int nmine = (active && vb0 < nv) ? (nv - 1 - vb0) / vstep + 1 : 0;
+  float ku = 0.f, kv = 0.f;
+  int64_t ko = 0;
+  bool kval = false;
+  for (int i = 0; i < nmine; ++i) {
+    const int vb = vb0 + i * vstep;
+    fin_lat_vblock(p, scr[grp], vb, gt, kBarFinGroup0 + grp, ku, kv, ko, kval);
+    // one virtual block: the values stay in registers until the norm is known; several: written
+    // unscaled now and rescaled (re-read by the same thread) after the norm barrier
+    if (kval && (nmine > 1 || p.mode == 2)) { p.out[ko] = ku; p.out[KD + ko] = kv; }
+  }
+  TRFF(12);
+  if (p.mode == 2) return;
+  // barrier 2: every part's norm published; each thread sums the parts in the same fixed order
+  __syncthreads();
+  if (tid == 0) grid_barrier(p.gbar, p.gbar + 32, (unsigned)ncta);
+  __syncthreads();
+  TRFF(13);
+  if (nmine == 0) return;
+  const int lane = tid & 31;
+  double n2 = 0.0;
+  for (int q = lane; q < nv; q += 32) n2 += __ldcg(p.norm2 + q);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, off);
+  const float sc = n2 > 0.0 ? (float)(1.0 / sqrt(n2)) : 1.f;
+  if (nmine == 1) {
+    if (kval) { p.out[ko] = ku * sc; p.out[KD + ko] = kv * sc; }
+    return;
+  }
+  for (int i = 0; i < nmine; ++i) {
+    const int vb = vb0 + i * vstep, bx = vb % lat_x, bz = vb / lat_x;
+    const int j = bx * kLatJ + (gt >> 3), k = bz * kLatK + (gt & (kLatK - 1));
+    if (k < p.D && j < p.K) {
+      float *o = p.out + (int64_t)j * p.D + k;
+      o[0] = o[0] * sc;
+      o[KD] = o[KD] * sc;
+    }
+  }
 }
 
 // a6 only: slots -> fp64 stats [N, S0, S1, S2] about c (reading A19).  Same grid as k_finalize.

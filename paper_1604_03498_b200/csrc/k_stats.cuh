@@ -33,6 +33,7 @@
 #include <cuda.h>
 
 #include "fv_common.cuh"
+#include "k_aux.cuh"
 #include "ptx.cuh"
 
 namespace gpufv {
@@ -68,6 +69,7 @@ constexpr int kNumBars = 16;
 constexpr int kS2Tmem = kS2Bar + kNumBars * 8;
 constexpr int kSmem2Bytes = kS2Tmem + 16 + 1024;
 static_assert(kSmem2Bytes <= 232448, "shared memory budget");
+static_assert(kLatGroups * sizeof(LatScratch) <= 2 * kOpBytes, "fused finalize scratch fits the P buffer");
 
 // barrier slots
 enum : int {
@@ -256,8 +258,12 @@ __device__ __forceinline__ void work_wait(uint64_t *bar, uint32_t parity) {
 // the 4 kC quarter pairs unroll without predicates (~3 % of the kernel's instructions at runtime C;
 // C4 k_stats 8.62 -> 8.21 ms).  (A third parameter compiling the per-row hooks out measured 9.41 ms:
 // the register allocation of this 96-register kernel moves with any change — measure each one.)
-template <bool kD64, int kC>
-__global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ CUtensorMap tmap_x, const Stats2Params p) {
+// kFin: the single-frame latency instantiation — after its last fold every CTA takes part in the
+// frame's finalize (fin_lat_fused, k_aux.cuh: two grid barriers, no second kernel); `fin` is read only
+// there.  The throughput instantiations (kFin = false) are unchanged.
+template <bool kD64, int kC, bool kFin = false>
+__global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ CUtensorMap tmap_x, const Stats2Params p,
+                                                        const __grid_constant__ FinParams fin) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_base = smem_u32(smem_raw);
@@ -309,6 +315,27 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
   if (tid == 0) TRP(1);
+  // A single set's schedule is known without any table: its first tile's two X boxes are requested
+  // before the cluster sync (a local TMA into this CTA's own buffers needs no peer), so the HBM round
+  // trip overlaps the wait for the peer CTA (latency path)
+  // (kFin instantiations only: in the throughput kernel the extra live state grew the spill area
+  // 114 -> 214 bytes)
+  bool tile0_issued = false;
+  if (kFin && p.single_rows >= 0 && warp == kWarpTma && lane == 0) {
+    const int64_t T0 = (p.single_rows + kTileM - 1) / kTileM;
+    const int a = (int)((int64_t)cid * T0 / ncl), b = (int)((int64_t)(cid + 1) * T0 / ncl);
+    if (a < b) {
+      TileWalker tw0;
+      tw0.init(p, a, b);
+      const TileMeta m = tw0.meta();
+      s_meta[0] = m;
+      mbar_arrive_expect_tx(&bars[B_XFULL0], kXBoxBytes);
+      tma_load_2d(sX, &tmap_x, 0, m.row0, &bars[B_XFULL0]);
+      mbar_arrive_expect_tx(&bars[B_XFULL1], kXBoxBytes);
+      tma_load_2d(sZ, &tmap_x, 32, m.row0, &bars[B_XFULL1]);
+      tile0_issued = true;
+    }
+  }
   cluster_sync();
   if (tid == 0) TRP(2);
   griddep_launch_dependents();  // k_finalize may start its prologue
@@ -339,6 +366,13 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       };
       for (int i = 0; i < n; ++i, tw.next()) {
         const TileMeta m = tw.meta();
+        if (kFin && i == 0 && tile0_issued) {  // requested before the cluster sync (same metadata)
+          TRP(4);
+          twp.init(p, t0, t1);
+          for (int k = 0; k < 4; ++k) prefetch_l2(k);
+          prefetch_l2(4);
+          continue;
+        }
         s_meta[i & 3] = m;  // released to the WORK warps by the X_FULL phase completions below
         // box 0 (dims 0..31) after box 1 of the previous tile was released
         if (i >= 1) mbar_wait(&bars[B_XEMPTY1], (i - 1) & 1);
@@ -683,13 +717,18 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   tc_fence_before();
   __syncthreads();
   if (tid == 0) TRP(8);
+  if constexpr (kFin) {
+    // the frame's finalize: the P / Z buffers are free (every GEMM2 and fold is done)
+    if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+    fin_lat_fused(fin, reinterpret_cast<LatScratch *>(smem + kS2P));
+  }
   cluster_sync();
   if (tid == 0) TRP(9);
 #ifdef GPUFV_TRACE
   if (p.trace && cid == 0 && rank == 0 && tid == 0) p.trace[7721] = ptx::globaltimer();
   if (p.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long *>(p.trace + 7722), (unsigned long long)ptx::globaltimer());
 #endif
-  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+  if (!kFin && warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
 }  // namespace gpufv

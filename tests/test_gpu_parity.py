@@ -326,34 +326,49 @@ _FUSED_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 import fvgen, paper_1604_03498_b200 as fv
-gmm_np = fvgen.make_gmm(256, 64, seed=1604)
-g = fv.GMM(*gmm_np)
 outs = []
-for n, seed in ((5000, 901), (129, 902), (17714, 903)):
-    X = torch.from_numpy(fvgen.make_descriptors(gmm_np, n, seed=seed)).cuda()
-    outs.append(fv.encode(X, g, threshold=1e-6).cpu().numpy())
-    off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
-    outs.append(fv.encode_batched(X, off, g, threshold=0.0).cpu().numpy()[0])
-np.save(sys.argv[2], np.stack([o.ravel() for o in outs]))
+for K, D in ((256, 64), (128, 36)):
+    gmm_np = fvgen.make_gmm(K, D, seed=1604)
+    g = fv.GMM(*gmm_np)
+    for n, seed in ((5000, 901), (129, 902), (17714, 903), (1000, 904)):
+        X = torch.from_numpy(fvgen.make_descriptors(gmm_np, n, seed=seed)).cuda()
+        outs.append(fv.encode(X, g, threshold=1e-6).cpu().numpy())
+        off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
+        outs.append(fv.encode_batched(X, off, g, threshold=0.0).cpu().numpy()[0])
+        for mode in (fv.NORM_POWER_L2, fv.NORM_NONE):
+            outs.append(fv.encode(X, g, threshold=1e-6, mode=mode).cpu().numpy())
+np.save(sys.argv[2], np.concatenate([o.ravel() for o in outs]))
 """
 
 
 def test_fused_schedule_equals_separate_schedule(fv, tmp_path):
     """Single-frame calls run without k_schedule (k_stats writes the finalize's tables, per-CTA range
-    flags): the FVs are bitwise those of the path with the separate schedule kernel (GPUFV_FUSED_SCHED=0,
-    read once per process, hence subprocesses) — fv_encode and one-image fv_encode_batched, one tile, a
-    ragged tile and the paper's 17,714-descriptor geometry."""
+    flags) and, by default, without a finalize kernel (every stats CTA takes part in the frame's
+    finalize after a grid barrier, fin_lat_fused): the FVs are bitwise those of the path with the
+    separate schedule and finalize kernels (GPUFV_FUSED_SCHED=0 / GPUFV_FIN_FUSED=0, read once per
+    process, hence subprocesses) — fv_encode and one-image fv_encode_batched, one tile, a ragged tile,
+    the paper's 17,714-descriptor geometry, all three normalisation modes, K = 128 (clusters of one CTA)
+    at D = 36; the fused finalize forced on (GPUFV_FIN_FUSED=2) at one and two tiles per cluster (two:
+    fewer CTAs than finalize blocks, so each CTA finalizes several blocks in turn).  The default (auto)
+    path is checked against the oracle by the encode parity tests."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for flag in ("0", "1"):
-        path = str(tmp_path / f"fused{flag}.npy")
-        r = subprocess.run([sys.executable, "-c", _FUSED_SCRIPT, root, path],
-                           env=dict(os.environ, GPUFV_FUSED_SCHED=flag), capture_output=True, text=True,
+    variants = {"separate": dict(GPUFV_FUSED_SCHED="0", GPUFV_FIN_FUSED="0"), "sched": dict(GPUFV_FIN_FUSED="0"),
+                "forced_2tile": dict(GPUFV_FIN_FUSED="2", GPUFV_MIN_TILES="2"),
+                "sched_1tile": dict(GPUFV_MIN_TILES="1", GPUFV_FIN_FUSED="0"),
+                "forced_1tile": dict(GPUFV_FIN_FUSED="2", GPUFV_MIN_TILES="1"), "auto": {}}
+    for name, extra in variants.items():
+        path = str(tmp_path / f"{name}.npy")
+        env = {k: v for k, v in os.environ.items() if not k.startswith("GPUFV_")}
+        env.update(extra)
+        r = subprocess.run([sys.executable, "-c", _FUSED_SCRIPT, root, path], env=env, capture_output=True, text=True,
                            timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
-        res[flag] = np.load(path)
-    assert np.array_equal(res["0"], res["1"])
-    assert np.all(np.isfinite(res["1"]))
+        res[name] = np.load(path)
+    assert np.array_equal(res["separate"], res["sched"])         # fused schedule == k_schedule
+    assert np.array_equal(res["sched"], res["forced_2tile"])     # fused finalize, several blocks per CTA
+    assert np.array_equal(res["sched_1tile"], res["forced_1tile"])  # fused finalize, one tile per cluster
+    assert np.all(np.isfinite(res["auto"])) and np.all(np.isfinite(res["forced_2tile"]))

@@ -72,7 +72,9 @@ for k, name in [(20, "k_stats CTA 0 entry"), (21, "k_stats CTA 0 end"), (22, "k_
                 (0, "k_finalize block 0 entry"), (1, "k_finalize griddep_wait returned"),
                 (8, "k_finalize segment loop start"), (5, "k_finalize segment loads summed"),
                 (6, "k_finalize S0 barrier passed"), (2, "k_finalize tile computed"), (3, "k_finalize image norm known (all blocks)"),
-                (4, "k_finalize block 0 end")]:
+                (4, "k_finalize block 0 end"),
+                (10, "fused finalize: CTA 0 enters"), (11, "fused finalize: barrier 1 passed"),
+                (12, "fused finalize: CTA 0 blocks computed"), (13, "fused finalize: barrier 2 passed")]:
     if G[k]:
         print(f"  {name:42s} {G[k] - g0:8d}")
 if G[23]:
