@@ -407,10 +407,15 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps k_schedule
   attr[1].val.programmaticStreamSerializationAllowed = 1;
-  static const bool coop_env = [] { const char *e = std::getenv("GPUFV_COOP"); return !(e && e[0] == '0'); }();
-  if (fin && coop_env) {  // fused finalize: its grid barriers need every CTA resident — a cooperative
-    attr[1].id = cudaLaunchAttributeCooperative;  // launch fails instead of hanging if the grid cannot be
-    attr[1].val.cooperative = 1;                  // (fin implies fuse: no programmatic serialization)
+  // Fused finalize: its grid barriers need every CTA resident.  The grid is at most the occupancy
+  // query's cluster count (one wave on an idle GPU — the assumption k_finalize_lat's and k_finalize<..,
+  // true>'s sibling waits already make).  GPUFV_COOP=1 adds the cooperative-launch attribute, which
+  // turns a grid that cannot be co-resident into a launch error; it is opt-in because Nsight Compute
+  // cannot profile a cooperative cluster launch (the process dies under ncu).
+  static const bool coop_env = [] { const char *e = std::getenv("GPUFV_COOP"); return e && e[0] == '1'; }();
+  if (fin && coop_env) {
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;  // (fin implies fuse: no programmatic serialization)
   }
   const FinParams fin_none{};
   const FinParams &fp = fin ? *fin : fin_none;

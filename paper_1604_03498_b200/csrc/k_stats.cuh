@@ -620,7 +620,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
         const int nr1 = s_meta[(i + 1) & 3].nrows;
         const float ssum = exp_local();
         zr_box<true>(xbox, row, 0, h, D, row < nr1, s_sc, s_ncs, tmem + kTZr + 128 * ((i + 1) & 1) + lane_base);
-        send(ssum);
+        send(ssum);  // (sending before the conversion measured -1.8 % on C4: the conversion then no
+                     // longer fills the exponentials' issue gaps)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars[B_XEMPTY0]);  // box 1 streams in behind the exchange below

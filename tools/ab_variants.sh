@@ -13,7 +13,7 @@ case $wl in
 esac
 for rep in $(seq $reps); do
 for v in $vs; do
-  cp variants/lib_$v.so paper_1604_03498_b200/libgpufv.so
+  cp ${VDIR:-variants}/lib_$v.so paper_1604_03498_b200/libgpufv.so
   a=$(timeout 300 python bench.py $args 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(round(d['value']/1e9,4), round(d['ms_per_step'],3), d['clocks'].get('sm_mhz'), d['clocks'].get('reasons'))")
   echo "$rep $v $wl: $a"
 done; done

@@ -12,7 +12,7 @@ import sys
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 g = os.path.join(root, "gpurun_out")
-out_dir = os.path.join(root, "profiles")
+out_dir = os.environ.get("NCU_SUMMARY_OUT", os.path.join(root, "profiles"))
 os.makedirs(out_dir, exist_ok=True)
 
 # ---- launch list: per-kernel share of device time (cold-cache, serialised: shares, not absolutes)
