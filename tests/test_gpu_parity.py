@@ -372,3 +372,25 @@ def test_fused_schedule_equals_separate_schedule(fv, tmp_path):
     assert np.array_equal(res["sched"], res["forced_2tile"])     # fused finalize, several blocks per CTA
     assert np.array_equal(res["sched_1tile"], res["forced_1tile"])  # fused finalize, one tile per cluster
     assert np.all(np.isfinite(res["auto"])) and np.all(np.isfinite(res["forced_2tile"]))
+
+
+def test_fused_finalize_workspace_reuse(fv):
+    """The fused finalize's grid barrier lives in the prepared GMM head and must reset itself: a chain
+    of single-frame calls of different sizes and modes on ONE prepared workspace (fused and two-kernel
+    paths interleaved, one barrier per call in NORM_NONE mode, two otherwise) gives bitwise the FVs of
+    fresh-workspace calls, and the fused sizes match the oracle."""
+    gmm_np = fvgen.make_gmm(256, 64, seed=1604)
+    gmm = fv.GMM(*gmm_np)
+    ws = fv.Workspace()
+    ws.ensure(fv.workspace_bytes(20000, 1, 256, 64))
+    fv.gmm_prepare(gmm, ws)
+    seq = [(5000, fv.NORM_IMPROVED), (8000, fv.NORM_IMPROVED), (129, fv.NORM_IMPROVED), (5000, fv.NORM_NONE),
+           (17714, fv.NORM_IMPROVED), (6000, fv.NORM_POWER_L2), (5000, fv.NORM_NONE), (8000, fv.NORM_IMPROVED)] * 2
+    data = {n: fvgen.make_descriptors(gmm_np, n, seed=700 + n) for n, _ in seq}
+    for n, mode in seq:
+        X = dev(data[n])
+        a = fv.encode(X, gmm, threshold=TAU, mode=mode, ws=ws, prepared=True).cpu().numpy()
+        b = fv.encode(X, gmm, threshold=TAU, mode=mode).cpu().numpy()
+        assert np.array_equal(a, b), (n, mode)
+        if mode == fv.NORM_IMPROVED and n in (5000, 8000):
+            assert rel_l2(a, oracle.encode(data[n], *gmm_np, threshold=TAU)) <= FV_RTOL
