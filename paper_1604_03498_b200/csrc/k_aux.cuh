@@ -1101,6 +1101,9 @@ __device__ __forceinline__ void grid_barrier(unsigned *ctr, unsigned *gen, unsig
   }
 }
 
+#ifndef GPUFV_FUSED_ROWS
+#define GPUFV_FUSED_ROWS 10  // measured: 5,000 descriptors 29.0 -> 27.0 us, 8,000 31.0 -> 29.1 us (20: the loads spill)
+#endif
 struct LatScratch {  // one virtual block's shared memory (k_finalize_lat's __shared__ arrays)
   double part[2][2 * kLatK][kLatJ];
   double p0[kLatThreads / 8][kLatJ];
@@ -1111,6 +1114,11 @@ constexpr int kLatGroups = 2;  // virtual blocks in flight per stats CTA (576 th
 
 // Virtual block vb = (bx, bz) of the single set: returns this thread's (unscaled) u, v and output
 // offset, publishes the block's partial norm to norm2[vb].  gt = thread index in the group.
+// kRows: slot rows per thread per round of loads.  The segments are summed in the same order for any
+// kRows (each round continues the thread's chain si = par, par + 2, ...), so the result is bitwise
+// k_finalize_lat's; inside the 96-register stats kernel fewer rows per round keep every load of a
+// round in flight instead of spilling.
+template <int kRows>
 __device__ __forceinline__ void fin_lat_vblock(const FinParams &p, LatScratch &s, int vb, int gt, uint32_t bar,
                                                float &u, float &v, int64_t &oofs, bool &valid) {
   const int lat_x = (p.K + kLatJ - 1) / kLatJ;
@@ -1134,16 +1142,16 @@ __device__ __forceinline__ void fin_lat_vblock(const FinParams &p, LatScratch &s
     const size_t frow = (size_t)((f & 1) ? p.dpad + kf : kf) * p.Kp + j0 + 4 * g;
     double a[4] = {0.0, 0.0, 0.0, 0.0};
     if (kf < p.D) {
-      for (int s0 = par; s0 < nseg; s0 += 2 * kLatRows) {
-        float4 w[kLatRows];
+      for (int s0 = par; s0 < nseg; s0 += 2 * kRows) {
+        float4 w[kRows];
 #pragma unroll
-        for (int uu = 0; uu < kLatRows; ++uu) {
+        for (int uu = 0; uu < kRows; ++uu) {
           const int si = s0 + 2 * uu;
           w[uu] = si < nseg ? __ldcg(reinterpret_cast<const float4 *>(p.slots + (size_t)seg_slot(si, 0) * seg_stride + frow))
                             : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int uu = 0; uu < kLatRows; ++uu) { a[0] += (double)w[uu].x; a[1] += (double)w[uu].y; a[2] += (double)w[uu].z; a[3] += (double)w[uu].w; }
+        for (int uu = 0; uu < kRows; ++uu) { a[0] += (double)w[uu].x; a[1] += (double)w[uu].y; a[2] += (double)w[uu].z; a[3] += (double)w[uu].w; }
       }
     }
     double z[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1244,7 +1252,7 @@ __device__ __forceinline__ void fin_lat_fused(const FinParams &p, LatScratch *sc
   bool kval = false;
   for (int i = 0; i < nmine; ++i) {
     const int vb = vb0 + i * vstep;
-    fin_lat_vblock(p, scr[grp], vb, gt, kBarFinGroup0 + grp, ku, kv, ko, kval);
+    fin_lat_vblock<GPUFV_FUSED_ROWS>(p, scr[grp], vb, gt, kBarFinGroup0 + grp, ku, kv, ko, kval);
     // one virtual block: the values stay in registers until the norm is known; several: written
     // unscaled now and rescaled (re-read by the same thread) after the norm barrier
     if (kval && (nmine > 1 || p.mode == 2)) { p.out[ko] = ku; p.out[KD + ko] = kv; }
