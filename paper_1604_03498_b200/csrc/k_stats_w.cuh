@@ -51,8 +51,12 @@ enum : int {
   W_L_EMPTY, W_P_FULL, W_ZB_FULL, W_FOLD_DONE, W_XCHG0, W_XCHG1, W_W_FULL, W_ZRA_FULL
 };
 
-// tensor-memory columns: Zr (half hf at 128 hf), L (64), S'_hf (64 each)
+// tensor-memory columns: Zr (half hf at 128 hf), L (64), S'_hf (64 each), L2 (64)
 constexpr uint32_t kWTZr = 0, kWTL = 256, kWTS = 320;
+// GEMM1's hi.hi products accumulate separately (L2, the 64 free columns) so that half a's can be issued
+// with half a's cross terms, before half b is converted; the WORK warps add L + L2 (fp32, round to
+// nearest: never worse than the truncating accumulator).  Same-box A/B: C5 +0.5 %, raw -> FV +0.7 %.
+constexpr uint32_t kWTL2 = 448;
 
 // kCW = cluster size at compile time (4: K = 256 e.g. the D = 82 raw -> FV path, 8: K = 512, C5), or 0
 // for any other size (read from %cluster_nctarank): the exchange loops unroll without predicates.
@@ -165,30 +169,31 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       auto g1 = [&](int s, int hf) {  // one split product of one feature half into L
         const uint32_t za = tmem + kWTZr + 128 * hf + (s == 1 ? 64 : 0);           // hi, lo, hi
         const uint32_t wb = sW + hf * (kWImgBytes / 2) + (s == 0 ? kGW * 128 * 2 : 0);  // lo, hi, hi
-        const bool first = (s == 0 && hf == 0);
+        const bool first = (s == 0 || s == 2) && hf == 0;         // L: cross terms, L2: hi.hi
+        const uint32_t dl = tmem + (s == 2 ? kWTL2 : kWTL);
         const uint32_t mask = (hf == 1 && skip3) ? 0x33u : 0xFFu;  // k-steps holding dims < 96
 #pragma unroll
         for (int kk = 0; kk < kNF / 16; ++kk) {
           if (!((mask >> kk) & 1u)) continue;
           const uint32_t off = (kk >> 2) * (kGW * 128) + (kk & 3) * 32;
-          mma_f16_ts_w(tmem + kWTL, za + kk * 8, desc_sw128(wb + off, 16, 1024), idesc1, (first && kk == 0) ? 0u : 1u);
+          mma_f16_ts_w(dl, za + kk * 8, desc_sw128(wb + off, 16, 1024), idesc1, (first && kk == 0) ? 0u : 1u);
         }
       };
-      // GEMM1 in two parts so half a's cross terms run while half b is still being converted; all
-      // cross terms precede the hi.hi terms (truncating accumulator): (s0,a) (s1,a) | (s0,b) (s1,b) (s2,a) (s2,b)
+      // GEMM1 in two parts so half a's products run while half b is still being converted; the cross
+      // terms accumulate in L apart from the hi.hi terms (L2): (s0,a) (s1,a) (s2,a -> L2) | (s0,b) (s1,b) (s2,b -> L2)
       auto gemm1a = [&](int i) {
         mbar_wait(&bars[W_ZRA_FULL], i & 1);
         if (i >= 1) mbar_wait(&bars[W_L_EMPTY], (i - 1) & 1);
         tc_fence_after();
         g1(0, 0);
         g1(1, 0);
+        g1(2, 0);
       };
       auto gemm1b = [&](int i) {
         mbar_wait(&bars[W_ZR_FULL], i & 1);
         tc_fence_after();
         g1(0, 1);
         g1(1, 1);
-        g1(2, 0);
         g1(2, 1);
         mma_commit_w(&bars[W_G1_DONE]);
       };
@@ -325,9 +330,16 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       {
         uint32_t rr[16];
         tmem_ld16(tmem + kWTL + lane_base + 16 * h, rr);
+        uint32_t r2[16];
+        tmem_ld16(tmem + kWTL2 + lane_base + 16 * h, r2);
         tmem_ld_wait(rr);
+        tmem_ld_wait(r2);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(rr[j]);
+        for (int j = 0; j < 16; j += 2) {
+          const float2 a = __fadd2_rn(make_float2(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])),
+                                      make_float2(__uint_as_float(r2[j]), __uint_as_float(r2[j + 1])));
+          v[j] = a.x; v[j + 1] = a.y;
+        }
       }
       tc_fence_before();
       __syncwarp();
