@@ -1,8 +1,11 @@
-# same-box latency A/B of the single-frame path variants (tools/latency_probe.py), alternated
+# same-box latency A/B of the single-frame path settings (tools/latency_probe.py), alternated
+# usage: bash tools/lat_ab.sh ["ENV=.. ENV=..;ENV=.."] ["N N .."] [reps]
 set -u
-for rep in 1 2; do
-for cfg in "GPUFV_FIN_FUSED=0" "GPUFV_FIN_FUSED=1" ; do
-  for n in 5000 8000 17714; do
+IFS=';' read -ra cfgs <<< "${1:-GPUFV_FIN_FUSED=0;GPUFV_FIN_FUSED=1}"
+ns=${2:-"5000 8000 17714"}; reps=${3:-2}
+for rep in $(seq $reps); do
+for cfg in "${cfgs[@]}"; do
+  for n in $ns; do
     echo -n "$cfg N=$n: "; env $cfg PROBE_N=$n timeout 120 python tools/latency_probe.py 2>&1 | tail -1
   done
 done
