@@ -81,7 +81,12 @@ size_t fv_workspace_bytes_host(int64_t n_total, int batch, int K, int D, unsigne
 fv_status fv_gmm_prepare(const float *weights /*K*/, const float *means /*KxD*/, const float *sigmas /*KxD*/,
                          int K, int D, unsigned flags, void *ws, size_t ws_bytes, fv_stream_t stream);
 
-/* One descriptor set X (N x D row-major) -> out (2KD).  N == 0 gives an all-zero FV (A11). */
+/* One descriptor set X (N x D row-major) -> out (2KD).  N == 0 gives an all-zero FV (A11).
+ * Latency path (D <= 64, K <= 256, a frame small enough for one tile per cluster): ONE kernel launch —
+ * the finalize runs inside the statistics kernel after a grid-wide barrier whose two words live in the
+ * prepared head of `ws` (zeroed by the GMM preparation, back to zero after every call).  Its CTAs must
+ * all be resident at once (at most the co-resident cluster count is launched; on a GPU shared with
+ * other work the call waits for SMs to free up).  The same holds for one-image fv_encode_batched. */
 fv_status fv_encode(const float *X, int64_t N, int D, const float *weights, const float *means,
                     const float *sigmas, int K, float threshold, unsigned flags, float *out,
                     void *ws, size_t ws_bytes, fv_stream_t stream);
