@@ -90,3 +90,28 @@ def test_random_em_steps(fv, seed):
     pi_r, mu_r, var_r, ll_r = oracle.em_step(X, *g)
     assert abs(float(ll.item()) - ll_r) <= 2e-5 * N
     assert np.abs(new.weights.cpu().numpy() - pi_r).max() <= 1e-5
+
+
+@pytest.mark.parametrize("seed", list(range(16)))
+def test_random_single_frames_match_oracle(fv, seed):
+    """Random single frames through fv_encode on the latency path — sizes spanning the fused-finalize
+    window (one tile per cluster, a CTA per finalize block) and its edges, narrow K / D, every mode and
+    tau — against the oracle; a repeat on the same workspace is bitwise equal."""
+    rng = np.random.default_rng(9000 + seed)
+    K = int(rng.choice([16, 32, 64, 100, 128, 129, 200, 256]))
+    D = int(4 * rng.integers(1, 17))                      # 4 .. 64
+    N = int(rng.choice([1, 127, 128, 1000, 4096, 4097, 5000, 6400, 8191, 9472, 9473, 12000]))
+    tau = float(rng.choice([0.0, 1e-6]))
+    mode = int(rng.choice([0, 1, 2]))
+    pi, mu, var = fvgen.make_gmm(K, D, seed=9100 + seed)
+    X = fvgen.make_descriptors((pi, mu, var), N, seed=9200 + seed)
+    gmm = fv.GMM(pi, mu, var)
+    ws = fv.Workspace()
+    Xd = torch.from_numpy(X).cuda()
+    a = fv.encode(Xd, gmm, threshold=tau, mode=mode, ws=ws).cpu().numpy()
+    b = fv.encode(Xd, gmm, threshold=tau, mode=mode, ws=ws, prepared=True).cpu().numpy()
+    assert np.array_equal(a, b)
+    ref = oracle.encode(X, pi, mu, var, threshold=tau, mode=mode)
+    nr = np.linalg.norm(ref)
+    err = np.linalg.norm(a - ref) / (nr if nr > 0 else 1.0)
+    assert np.all(np.isfinite(a)) and err <= 1e-4, f"K={K} D={D} N={N} tau={tau} mode={mode}: {err:.2e}"
