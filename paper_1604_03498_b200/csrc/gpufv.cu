@@ -103,9 +103,10 @@ int gauss_per_cta(int K, int D) { return is_wide(K, D) ? kGW : kG; }
 int cluster_size(int K, int D) { return (K + gauss_per_cta(K, D) - 1) / gauss_per_cta(K, D); }
 // Fused finalize for a single narrow frame (auto mode) only when the frame has one tile per cluster and
 // every one of the finalize's (K/32) x (D/8) blocks gets a CTA of its own.  Measured (same box, p50):
-// 5,000 descriptors 29.0 vs 30.1-32 us (the separate k_finalize_lat); with fewer CTAs than blocks each
-// CTA finalizes several in turn (1,000 descriptors: 37 vs 31 us), and with more tiles than clusters
-// the extra segments cost more than the saved launch (10,000: 35 vs 31 us; 17,714: 35 vs 34 us).
+// 5,000 descriptors 27.0 vs 30.1-32 us (the separate k_finalize_lat), 8,000: 29.1 vs 30.1-31; with
+// fewer CTAs than blocks each CTA finalizes several in turn (1,000 descriptors: 37 vs 31 us), and with
+// more tiles than clusters the extra segments cost more than the saved launch (two tiles per cluster,
+// forced: 10,000 31.1 vs 31.2 us, 17,714 35.2 vs 34.2, 40,000 45.6 vs 45.0).
 bool fin_fused_wanted(int K, int D, int n_cls, int C, int64_t ncl, int64_t tiles, int64_t ncl_max) {
   const int mode = fin_fused_mode();
   if (mode == 0 || is_wide(K, D) || n_cls != 0 || !lat_finalize_fits(K, D, 1)) return false;
@@ -197,8 +198,7 @@ bool make_layout(int64_t n_total, int batch, int K, int D, bool host_io, Layout 
   const int64_t tmax = batch == 1 ? (n_total + kTileM - 1) / kTileM : n_total / kTileM + batch;
   int mt = min_tiles_per_cluster();
   // A single frame whose finalize runs inside k_stats: one tile per cluster — the finalize's (K/32) x
-  // (D/8) blocks then land on distinct SMs (measured, 5,000 descriptors: 33.2 us at 2 tiles per
-  // cluster, 27.0-27.8 at 1; the separate-kernel path 31-32 at either)
+  // (D/8) blocks then land on distinct SMs and each cluster leaves one segment per tile (fin_fused_wanted)
   if (batch == 1 && min_tiles_env() == 0 && fin_fused_mode() == 1 &&
       fin_fused_wanted(K, D, n_cls, L.C, std::min<int64_t>(L.ncl, tmax), tmax, L.ncl))
     mt = 1;
