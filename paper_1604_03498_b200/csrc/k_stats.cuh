@@ -315,27 +315,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
   if (tid == 0) TRP(1);
-  // A single set's schedule is known without any table: its first tile's two X boxes are requested
-  // before the cluster sync (a local TMA into this CTA's own buffers needs no peer), so the HBM round
-  // trip overlaps the wait for the peer CTA (latency path)
-  // (kFin instantiations only: in the throughput kernel the extra live state grew the spill area
-  // 114 -> 214 bytes)
-  bool tile0_issued = false;
-  if (kFin && p.single_rows >= 0 && warp == kWarpTma && lane == 0) {
-    const int64_t T0 = (p.single_rows + kTileM - 1) / kTileM;
-    const int a = (int)((int64_t)cid * T0 / ncl), b = (int)((int64_t)(cid + 1) * T0 / ncl);
-    if (a < b) {
-      TileWalker tw0;
-      tw0.init(p, a, b);
-      const TileMeta m = tw0.meta();
-      s_meta[0] = m;
-      mbar_arrive_expect_tx(&bars[B_XFULL0], kXBoxBytes);
-      tma_load_2d(sX, &tmap_x, 0, m.row0, &bars[B_XFULL0]);
-      mbar_arrive_expect_tx(&bars[B_XFULL1], kXBoxBytes);
-      tma_load_2d(sZ, &tmap_x, 32, m.row0, &bars[B_XFULL1]);
-      tile0_issued = true;
-    }
-  }
   cluster_sync();
   if (tid == 0) TRP(2);
   griddep_launch_dependents();  // k_finalize may start its prologue
@@ -366,13 +345,6 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats(const __grid_constant__ 
       };
       for (int i = 0; i < n; ++i, tw.next()) {
         const TileMeta m = tw.meta();
-        if (kFin && i == 0 && tile0_issued) {  // requested before the cluster sync (same metadata)
-          TRP(4);
-          twp.init(p, t0, t1);
-          for (int k = 0; k < 4; ++k) prefetch_l2(k);
-          prefetch_l2(4);
-          continue;
-        }
         s_meta[i & 3] = m;  // released to the WORK warps by the X_FULL phase completions below
         // box 0 (dims 0..31) after box 1 of the previous tile was released
         if (i >= 1) mbar_wait(&bars[B_XEMPTY1], (i - 1) & 1);
