@@ -396,6 +396,22 @@ def run_legs(fv, gmm, gmm_np, dev, stream, rank, world, Xd_c4=None, offs_c4=None
     legs["c1"] = {"eager_us": latency_us(one, dev, stream)}
     legs["c1"]["graph_us"] = graph_latency_us(one, dev, stream)
     legs["c1"]["workload"] = f"C1: one image, {c1['counts'][0]} descriptors, K={c1['K']}, D={c1['D']}, exact"
+    # the monitoring application per frame: one C2 frame -> one linear score, the FV
+    # never written (fv_encode_scored_batched, batch 1: the scores come out of the single-kernel path)
+    if Xd_c4 is not None:
+        xs = Xd_c4[:PER_FRAME].contiguous()
+        offs1 = torch.tensor([0, PER_FRAME], dtype=torch.int64, device=dev)
+        wcls = torch.from_numpy(np.random.default_rng(5).standard_normal((1, 2 * K * D)).astype(np.float32)).to(dev)
+        wss = fv.Workspace(device=dev)
+        fv.encode_scored_batched(xs, offs1, gmm, wcls, None, threshold=TAU, ws=wss)
+        fv.gmm_prepare(gmm, wss)
+
+        def scored():
+            fv.encode_scored_batched(xs, offs1, gmm, wcls, None, threshold=TAU, ws=wss, prepared=True)
+        legs["scored_frame"] = {"eager_us": latency_us(scored, dev, stream),
+                                "graph_us": graph_latency_us(scored, dev, stream),
+                                "workload": f"one frame, {PER_FRAME} descriptors, K={K}, D={D}, tau={TAU}, "
+                                            "1 class; scores only (FV not written)"}
     return legs
 
 

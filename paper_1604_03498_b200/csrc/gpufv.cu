@@ -109,7 +109,7 @@ int cluster_size(int K, int D) { return (K + gauss_per_cta(K, D) - 1) / gauss_pe
 // forced: 10,000 31.1 vs 31.2 us, 17,714 35.2 vs 34.2, 40,000 45.6 vs 45.0).
 bool fin_fused_wanted(int K, int D, int n_cls, int C, int64_t ncl, int64_t tiles, int64_t ncl_max) {
   const int mode = fin_fused_mode();
-  if (mode == 0 || is_wide(K, D) || n_cls != 0 || !lat_finalize_fits(K, D, 1)) return false;
+  if (mode == 0 || is_wide(K, D) || n_cls > kMaxCls || !lat_finalize_fits(K, D, 1)) return false;
   if (mode >= 2) return true;
   const int nv = ((K + kLatJ - 1) / kLatJ) * ((D + kLatK - 1) / kLatK);
   return tiles <= ncl_max && ncl == tiles && (int64_t)C * ncl >= nv;
@@ -607,8 +607,16 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   // launch on the latency path; GPUFV_FUSED_SCHED=0 keeps the separate kernel, for A/B runs)
   static const bool fuse_env = [] { const char *e = std::getenv("GPUFV_FUSED_SCHED"); return !(e && e[0] == '0'); }();
   // (every cluster must own a tile: the finalize takes clusters 0 .. ncl-1 as the set's segments)
-  const bool fuse = fuse_env && batch == 1 && rows < 0 && n_total > 0 && !sparse && !is_wide(K, D) && sc.n_cls == 0 &&
-                    lat_finalize_fits(K, D, batch) && (int64_t)L.ncl <= (n_total + kTileM - 1) / kTileM;
+  const bool fuse_ok = fuse_env && batch == 1 && rows < 0 && n_total > 0 && !sparse && !is_wide(K, D) &&
+                       lat_finalize_fits(K, D, batch) && (int64_t)L.ncl <= (n_total + kTileM - 1) / kTileM;
+  // ... and its finalize runs inside k_stats (fin_lat_fused: no second kernel; GPUFV_FIN_FUSED=0 keeps
+  // k_finalize_lat, for A/B runs).  A scored frame (the monitoring application) takes the fused path
+  // only with its finalize fused (k_finalize_lat has no scoring) and an L2 norm (NORM_NONE scores stay
+  // on the two-kernel path)
+  const bool fin_fused = fuse_ok && (sc.n_cls == 0 || (flags & FV_NORM_MASK) != FV_NORM_NONE) &&
+                         fin_fused_wanted(K, D, sc.n_cls, L.C, L.ncl, (n_total + kTileM - 1) / kTileM,
+                                          num_clusters(L.C, false));
+  const bool fuse = fuse_ok && (sc.n_cls == 0 || fin_fused);
   FinParams f = fin_params(L, offsets, batch, K, D, w, mu, sg, flags, ws);
   if (fuse) {  // the finalize ORs the per-CTA range flags into the image's flag word and derives the
                // single set's segments (every cluster owns >= 1 of its T >= ncl tiles) and N itself
@@ -619,10 +627,6 @@ fv_status encode_batched_impl(const float *X, const int64_t *offsets, int batch,
   }
   f.out = out;
   f.svm_w = sc.w; f.svm_b = sc.b; f.n_cls = sc.n_cls; f.scores = sc.scores;
-  // ... and its finalize runs inside k_stats (fin_lat_fused: no second kernel; GPUFV_FIN_FUSED=0 keeps
-  // k_finalize_lat, for A/B runs)
-  const bool fin_fused = fuse && fin_fused_wanted(K, D, sc.n_cls, L.C, L.ncl, (n_total + kTileM - 1) / kTileM,
-                                                  num_clusters(L.C, false));
   if (fv_status s = launch_stats(L, X, offsets, n_total, batch, D, K, thr, ws, nullptr, 0, st, nullptr, ldx, rf_base, rows,
                                  sparse, fuse, fin_fused ? &f : nullptr))
     return s;

@@ -1109,6 +1109,7 @@ struct LatScratch {  // one virtual block's shared memory (k_finalize_lat's __sh
   double p0[kLatThreads / 8][kLatJ];
   double S0[kLatJ];
   double red[kLatThreads / 32];
+  float dot[kLatThreads / 32][kMaxCls];  // fused scoring: per-warp partial dot products
 };
 constexpr int kLatGroups = 2;  // virtual blocks in flight per stats CTA (576 threads: 2 x 256)
 
@@ -1200,15 +1201,37 @@ __device__ __forceinline__ void fin_lat_vblock(const FinParams &p, LatScratch &s
     }
   }
   oofs = (int64_t)j * p.D + k;
+  if (p.n_cls > 0) {  // fused scoring (NEXT-4): this block's dot products with the classifier rows, on
+                      // the FV before the L2 scale (k_finalize_img's order: U element, then V element)
+    const int KD = p.K * p.D;
+    for (int c = 0; c < p.n_cls; ++c) {
+      float a = 0.f;
+      if (valid) {
+        const float *wc = p.svm_w + (size_t)c * 2 * KD;
+        a = fmaf(u, __ldg(wc + oofs), a);
+        a = fmaf(v, __ldg(wc + KD + oofs), a);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if (lane == 0) s.dot[gt >> 5][c] = a;
+    }
+  }
   if (p.mode != 2) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
     if (lane == 0) s.red[gt >> 5] = ss;
+  }
+  if (p.mode != 2 || p.n_cls > 0) {
     ptx::named_bar_sync(bar, kLatThreads);
-    if (gt == 0) {
+    if (p.mode != 2 && gt == 0) {
       double tot = 0.0;
       for (int w = 0; w < kLatThreads / 32; ++w) tot += s.red[w];
       p.norm2[vb] = tot;
+    }
+    if (gt < p.n_cls) {  // the block's partial per class, fixed warp order (bitwise repeatable)
+      double d = 0.0;
+      for (int w = 0; w < kLatThreads / 32; ++w) d += (double)s.dot[w][gt];
+      p.spart[(size_t)vb * p.n_cls + gt] = d;
     }
   }
   ptx::named_bar_sync(bar, kLatThreads);  // the scratch is reused by the group's next virtual block
@@ -1255,10 +1278,10 @@ __device__ __forceinline__ void fin_lat_fused(const FinParams &p, LatScratch *sc
     fin_lat_vblock<GPUFV_FUSED_ROWS>(p, scr[grp], vb, gt, kBarFinGroup0 + grp, ku, kv, ko, kval);
     // one virtual block: the values stay in registers until the norm is known; several: written
     // unscaled now and rescaled (re-read by the same thread) after the norm barrier
-    if (kval && (nmine > 1 || p.mode == 2)) { p.out[ko] = ku; p.out[KD + ko] = kv; }
+    if (p.out && kval && (nmine > 1 || p.mode == 2)) { p.out[ko] = ku; p.out[KD + ko] = kv; }
   }
   TRFF(12);
-  if (p.mode == 2) return;
+  if (p.mode == 2) return;  // (no scoring in this mode: the host keeps it on the two-kernel path)
   // barrier 2: every part's norm published; each thread sums the parts in the same fixed order
   __syncthreads();
   if (tid == 0) grid_barrier(p.gbar, p.gbar + 32, (unsigned)ncta);
@@ -1271,6 +1294,13 @@ __device__ __forceinline__ void fin_lat_fused(const FinParams &p, LatScratch *sc
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, off);
   const float sc = n2 > 0.0 ? (float)(1.0 / sqrt(n2)) : 1.f;
+  if (p.n_cls > 0 && cta == 0 && tid < p.n_cls) {  // scores: the blocks' partials in block order
+    double d = 0.0;
+    for (int q = 0; q < nv; ++q) d += __ldcg(p.spart + (size_t)q * p.n_cls + tid);
+    const double inv = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;
+    p.scores[tid] = (float)(d * inv + (p.svm_b ? (double)p.svm_b[tid] : 0.0));
+  }
+  if (!p.out) return;
   if (nmine == 1) {
     if (kval) { p.out[ko] = ku * sc; p.out[KD + ko] = kv * sc; }
     return;

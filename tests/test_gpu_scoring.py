@@ -107,3 +107,26 @@ def test_scores_self_similarity(fv):
     gmm = fv.GMM(*gmm_np)
     s = fv.encode_scored_batched(dev(X), dev(off), gmm, dev(F_ref.astype(np.float32))).cpu().numpy()
     np.testing.assert_allclose(np.diag(s), 1.0, atol=2e-4)
+
+
+@pytest.mark.parametrize("n_cls", [1, 32])
+@pytest.mark.parametrize("tau,mode", [(0.0, oracle.NORM_IMPROVED), (1e-6, oracle.NORM_IMPROVED),
+                                      (1e-6, oracle.NORM_POWER_L2), (1e-6, oracle.NORM_NONE)])
+def test_single_frame_scores_latency_path(fv, n_cls, tau, mode):
+    """One monitoring frame (5,000 descriptors, the real-time use of P:563-564): the scores come out of
+    the single-kernel latency path (the finalize and the dot products inside k_stats; NORM_NONE stays on
+    the two-kernel path) within the Cauchy-Schwarz bound of the oracle; the returned FV is bitwise the
+    plain encode's; a scores-only call (no FV written) gives the same scores bitwise."""
+    K, D = 256, 64
+    gmm_np = fvgen.make_gmm(K, D, seed=1604)
+    X, off = fvgen.make_batch(gmm_np, [5000], seed_base=4700 + n_cls)
+    W, b = classifier(n_cls, 2 * K * D, seed=4800 + n_cls)
+    gmm = fv.GMM(*gmm_np)
+    s, F = fv.encode_scored_batched(dev(X), dev(off), gmm, dev(W), dev(b), threshold=tau, mode=mode, return_fv=True)
+    s, F = s.cpu().numpy(), F.cpu().numpy()
+    F_ref = oracle.encode_batched(X, off, *gmm_np, threshold=tau, mode=mode)
+    check_scores(s, F_ref, W, b, mode)
+    F2 = fv.encode_batched(dev(X), dev(off), gmm, threshold=tau, mode=mode).cpu().numpy()
+    np.testing.assert_array_equal(F2, F)
+    s2 = fv.encode_scored_batched(dev(X), dev(off), gmm, dev(W), dev(b), threshold=tau, mode=mode).cpu().numpy()
+    np.testing.assert_array_equal(s2, s)
