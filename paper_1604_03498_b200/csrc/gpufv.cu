@@ -788,8 +788,10 @@ fv_status encode_host_impl(const float *X_host, const int64_t *offsets_host, int
     Scoring sc = sc_in;
     float *out = dres + (size_t)b0 * per_image;
     if (sc.n_cls > 0) { sc.scores = out; out = nullptr; }
+    // (a one-image call is one set with offsets {0, n_total}, checked above: rows = -1 lets it take the
+    // single-kernel latency path like fv_encode)
     rs = encode_batched_impl(dX, doff + b0, b1 - b0, n_total, D, w, mu, sg, K, thr, flags | FV_PREPARED, out, ws,
-                             ws_bytes, st, &L, sc, 0, b0, r1 - r0);
+                             ws_bytes, st, &L, sc, 0, b0, batch == 1 ? -1 : r1 - r0);
     if (rs != FV_OK) break;
     cudaEventRecord(ev[2 * k + 1], st);
     cudaStreamWaitEvent(cout, ev[2 * k + 1], 0);

@@ -394,3 +394,20 @@ def test_fused_finalize_workspace_reuse(fv):
         assert np.array_equal(a, b), (n, mode)
         if mode == fv.NORM_IMPROVED and n in (5000, 8000):
             assert rel_l2(a, oracle.encode(data[n], *gmm_np, threshold=TAU)) <= FV_RTOL
+
+
+def test_host_entry_single_frame(fv):
+    """One frame through the host entry point (pinned host X in, FV out) takes the single-kernel
+    latency path like fv_encode: bitwise the device call's FV, and the scored variant's score."""
+    gmm_np = fvgen.make_gmm(256, 64, seed=1604)
+    X, off = fvgen.make_batch(gmm_np, [5000], seed_base=61)
+    gmm = fv.GMM(*gmm_np)
+    host = fv.encode_batched_host(torch.from_numpy(X).pin_memory(), torch.from_numpy(off), gmm, threshold=TAU).numpy()
+    devout = fv.encode(dev(X), gmm, threshold=TAU).cpu().numpy()
+    assert np.array_equal(host[0], devout)
+    assert rel_l2(host[0], oracle.encode(X, *gmm_np, threshold=TAU)) <= FV_RTOL
+    W = np.random.default_rng(3).standard_normal((2, 2 * 256 * 64)).astype(np.float32)
+    sh = fv.encode_scored_batched_host(torch.from_numpy(X).pin_memory(), torch.from_numpy(off), gmm, dev(W),
+                                       threshold=TAU).numpy()
+    sd = fv.encode_scored_batched(dev(X), dev(off), gmm, dev(W), threshold=TAU).cpu().numpy()
+    assert np.array_equal(sh, sd)
