@@ -95,17 +95,18 @@ def test_random_em_steps(fv, seed):
 @pytest.mark.parametrize("seed", list(range(16)))
 def test_random_single_frames_match_oracle(fv, seed):
     """Random single frames through fv_encode on the latency path — sizes spanning the fused-finalize
-    window (one tile per cluster, a CTA per finalize block) and its edges, narrow K / D, every mode and
-    tau — against the oracle; a repeat on the same workspace is bitwise equal."""
+    window (one tile per cluster, a CTA per finalize block) and its edges, narrow K / D, every mode, tau
+    and sigma convention — against the oracle; a repeat on the same workspace is bitwise equal."""
     rng = np.random.default_rng(9000 + seed)
     K = int(rng.choice([16, 32, 64, 100, 128, 129, 200, 256]))
     D = int(4 * rng.integers(1, 17))                      # 4 .. 64
     N = int(rng.choice([1, 127, 128, 1000, 4096, 4097, 5000, 6400, 8191, 9472, 9473, 12000]))
     tau = float(rng.choice([0.0, 1e-6]))
     mode = int(rng.choice([0, 1, 2]))
+    stddev = bool(rng.integers(0, 2))
     pi, mu, var = fvgen.make_gmm(K, D, seed=9100 + seed)
     X = fvgen.make_descriptors((pi, mu, var), N, seed=9200 + seed)
-    gmm = fv.GMM(pi, mu, var)
+    gmm = fv.GMM(pi, mu, np.sqrt(var).astype(np.float32) if stddev else var, stddev=stddev)
     ws = fv.Workspace()
     Xd = torch.from_numpy(X).cuda()
     a = fv.encode(Xd, gmm, threshold=tau, mode=mode, ws=ws).cpu().numpy()
@@ -114,4 +115,4 @@ def test_random_single_frames_match_oracle(fv, seed):
     ref = oracle.encode(X, pi, mu, var, threshold=tau, mode=mode)
     nr = np.linalg.norm(ref)
     err = np.linalg.norm(a - ref) / (nr if nr > 0 else 1.0)
-    assert np.all(np.isfinite(a)) and err <= 1e-4, f"K={K} D={D} N={N} tau={tau} mode={mode}: {err:.2e}"
+    assert np.all(np.isfinite(a)) and err <= 1e-4, f"K={K} D={D} N={N} tau={tau} mode={mode} sd={stddev}: {err:.2e}"
