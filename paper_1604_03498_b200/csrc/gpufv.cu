@@ -99,6 +99,12 @@ int fin_fused_mode() {
 bool lat_finalize_fits(int K, int D, int batch);
 bool fin_fused_wanted(int K, int D, int n_cls, int C, int64_t ncl, int64_t tiles, int64_t ncl_max);
 bool is_wide(int K, int D) { return D > kDP || K > kG * kMaxC2; }
+// Wide family with D <= 96 (the paper's 82-dim format): the second feature half packed into 64
+// features (k_stats_w<.., kPk>, W' by k_prep_w with wide == 2); GPUFV_WIDE_PACK=0 for A/B runs
+bool wide_packed(int K, int D) {
+  static const bool env = [] { const char *e = std::getenv("GPUFV_WIDE_PACK"); return !(e && e[0] == '0'); }();
+  return env && is_wide(K, D) && D <= 96;
+}
 int gauss_per_cta(int K, int D) { return is_wide(K, D) ? kGW : kG; }
 int cluster_size(int K, int D) { return (K + gauss_per_cta(K, D) - 1) / gauss_per_cta(K, D); }
 // Fused finalize for a single narrow frame (auto mode) only when the frame has one tile per cluster and
@@ -144,6 +150,12 @@ int num_clusters(int C, bool wide) {
       cudaFuncSetAttribute(k_stats_w<false, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_w<false, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_w<false, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 0, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 4, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 4, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(k_stats_w<false, 8, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_sp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSpBytes) != cudaSuccess ||
       cudaFuncSetAttribute(k_stats_sp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSpBytes) != cudaSuccess)
     return -1;
@@ -318,7 +330,8 @@ fv_status launch_prep(const Layout &L, const float *w, const float *mu, const fl
   k_prep_bias_final<<<1, 512, 0, st>>>(K, L.Kp, (const double *)at(ws, L.bscratch), (float *)at(ws, L.bias),
                                        (double *)at(ws, L.bmax));
   k_prep_w<<<L.Kp, 2 * L.dpad, 0, st>>>(mu, sg, K, D, sd, (const double *)at(ws, L.cshift), (const float *)at(ws, L.xscale),
-                                 at(ws, L.wimg), (double *)at(ws, L.coef), is_wide(K, D) ? 1 : 0, (int *)at(ws, L.gflag));
+                                 at(ws, L.wimg), (double *)at(ws, L.coef), wide_packed(K, D) ? 2 : is_wide(K, D) ? 1 : 0,
+                                 (int *)at(ws, L.gflag));
   g_launches += 4;
   return cuda_check("k_prep");
 }
@@ -442,8 +455,13 @@ fv_status launch_stats(const Layout &L, const float *X, const int64_t *&offsets,
          {k_stats_w<false, 8, false>, k_stats_w<false, 8, true>}},
         {{k_stats_w<true, 0, false>, k_stats_w<true, 0, true>}, {k_stats_w<true, 4, false>, k_stats_w<true, 4, true>},
          {k_stats_w<true, 8, false>, k_stats_w<true, 8, true>}}};
+    const KW kwp[3][2] = {{k_stats_w<false, 0, false, true>, k_stats_w<false, 0, true, true>},
+                          {k_stats_w<false, 4, false, true>, k_stats_w<false, 4, true, true>},
+                          {k_stats_w<false, 8, false, true>, k_stats_w<false, 8, true, true>}};
     const bool hooks = gamma != nullptr || loglik_rows != nullptr;
-    e = cudaLaunchKernelEx(&cfg, kw[D == kDMax][L.C == 8 ? 2 : L.C == 4 ? 1 : 0][hooks], tmap, p);
+    const int ci = L.C == 8 ? 2 : L.C == 4 ? 1 : 0;
+    e = wide_packed(K, D) ? cudaLaunchKernelEx(&cfg, kwp[ci][hooks], tmap, p)
+                          : cudaLaunchKernelEx(&cfg, kw[D == kDMax][ci][hooks], tmap, p);
   }
   if (g_prof_stop) cudaEventRecord(g_prof_stop, st);
   g_launches += 1;

@@ -142,8 +142,17 @@ __global__ void k_prep_w(const float *mu, const float *sg, int K, int D, int std
     const int hf = f / kNF, fh = f % kNF;
     lin = fh < kDP;
     k = kDP * hf + (fh & (kDP - 1));
-    const int rank = j / kGW, row = j % kGW, atom = fh / 64, chunk = (fh & 63) >> 3, e = fh & 7;
-    off = rank * kWImgBytes + hf * (kWImgBytes / 2) + atom * (kGW * 128) + row * 128 + ((chunk ^ (row & 7)) << 4) + e * 2;
+    // D <= 96 (packed second half, k_stats_w<.., kPk>): half b's 64 features [lin dims 64-95 | quad dims
+    // 64-95] fill its first atom; the coefficients of dims 96-127 (zero) are not stored
+    int pos = fh;
+    if (wide == 2 && hf == 1) pos = (fh & 63) < 32 ? (lin ? fh : 32 + (fh - kDP)) : -1;
+    const int rank = j / kGW, row = j % kGW;
+    if (pos >= 0) {
+      const int atom = pos / 64, chunk = (pos & 63) >> 3, e = pos & 7;
+      off = rank * kWImgBytes + hf * (kWImgBytes / 2) + atom * (kGW * 128) + row * 128 + ((chunk ^ (row & 7)) << 4) + e * 2;
+    } else {
+      off = -1;
+    }
   }
   const int lo_off = wide ? kGW * 128 * 2 : kOpBytes;  // lo half after the 2 hi atoms
   double wv = 0.0;
@@ -173,6 +182,7 @@ __global__ void k_prep_w(const float *mu, const float *sg, int K, int D, int std
   }
   const __half hi = __float2half_rn(w32);
   const __half lo = __float2half_rn(w32 - __half2float(hi));
+  if (off < 0) return;
   *reinterpret_cast<__half *>(wimg + off) = hi;
   *reinterpret_cast<__half *>(wimg + off + lo_off) = lo;
 }

@@ -193,7 +193,9 @@ __device__ __forceinline__ void warp_transpose_reduce32(float (&a)[32], int lane
 // Features of dims k = 32 box + 8h .. +8 of one row, from the staged box (dims [32 box, 32 box + 32),
 // 16-byte chunks 2h, 2h+1 of the row): linear hi -> Zr col k/2, quadratic hi -> col 32 + k/2,
 // lo -> + 64.  kMask: dims >= D or a row past the image end are zeroed.
-template <bool kMask>
+// kQO / kLO: column offsets of the quadratic hi and the linear lo words (the wide kernel's packed
+// second half for D <= 96 puts [lin | quad] of 32 dims each in 32 columns per hi / lo part: 16 / 32)
+template <bool kMask, int kQO = 32, int kLO = 64>
 __device__ __forceinline__ void zr_box(const uint8_t *xbox, int row, int box, int h, int D, bool valid,
                                        const float *s_sc, const float *s_ncs, uint32_t taddr) {
   using namespace ptx;
@@ -219,9 +221,9 @@ __device__ __forceinline__ void zr_box(const uint8_t *xbox, int row, int box, in
     split2_f16(__fmul2_rn(a1, a1), qh[2 * c2 + 1], ql[2 * c2 + 1]);
   }
   tmem_st4(taddr + k0 / 2, lh);
-  tmem_st4(taddr + 32 + k0 / 2, qh);
-  tmem_st4(taddr + 64 + k0 / 2, ll);
-  tmem_st4(taddr + 96 + k0 / 2, ql);
+  tmem_st4(taddr + kQO + k0 / 2, qh);
+  tmem_st4(taddr + kLO + k0 / 2, ll);
+  tmem_st4(taddr + kLO + kQO + k0 / 2, ql);
 }
 
 // A row whose log-likelihoods are not all finite — a descriptor outside the fp16 operand range

@@ -62,7 +62,11 @@ constexpr uint32_t kWTL2 = 448;
 // for any other size (read from %cluster_nctarank): the exchange loops unroll without predicates.
 // kHooks: the per-row posterior / log-likelihood outputs (fv_posteriors, the EM E-step) are compiled
 // in; the encode instantiations leave them out (+2.5 % C5, +1 % raw -> FV at D = 82, same-box A/B).
-template <bool kD128, int kCW, bool kHooks>
+// kPk (D <= 96, with kD128 = false): the second feature half holds only dims 64-95, packed as 64
+// features [lin | quad] in one atom — GEMM2b runs as M = 64 (its accumulator in lanes 0-15 of each
+// TMEM lane quarter, tools/m64_probe.cu), the Z_b copy and the half-b fold move half the data, and
+// k_prep_w stores W' half b in the same packed order (wide == 2)
+template <bool kD128, int kCW, bool kHooks, bool kPk = false>
 __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant__ CUtensorMap tmap_x, const Stats2Params p) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
@@ -167,11 +171,12 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       uint32_t folds = 0;
       mbar_wait(&bars[W_W_FULL], 0);
       auto g1 = [&](int s, int hf) {  // one split product of one feature half into L
-        const uint32_t za = tmem + kWTZr + 128 * hf + (s == 1 ? 64 : 0);           // hi, lo, hi
+        const bool pk = kPk && hf == 1;  // packed half b: 64 features, lo at column 32
+        const uint32_t za = tmem + kWTZr + 128 * hf + (s == 1 ? (pk ? 32 : 64) : 0);  // hi, lo, hi
         const uint32_t wb = sW + hf * (kWImgBytes / 2) + (s == 0 ? kGW * 128 * 2 : 0);  // lo, hi, hi
         const bool first = (s == 0 || s == 2) && hf == 0;         // L: cross terms, L2: hi.hi
         const uint32_t dl = tmem + (s == 2 ? kWTL2 : kWTL);
-        const uint32_t mask = (hf == 1 && skip3) ? 0x33u : 0xFFu;  // k-steps holding dims < 96
+        const uint32_t mask = pk ? 0x0Fu : (hf == 1 && skip3) ? 0x33u : 0xFFu;  // k-steps holding dims < 96
 #pragma unroll
         for (int kk = 0; kk < kNF / 16; ++kk) {
           if (!((mask >> kk) & 1u)) continue;
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         mma_commit_w(&bars[W_G1_DONE]);
       };
       auto gemm1 = [&](int i) { gemm1a(i); gemm1b(i); };
+      const uint32_t idesc2b = idesc_f16_f32(kPk ? kNF / 2 : kNF, kGW, 1, 1);  // packed half b: M = 64
       auto gemm2 = [&](int hf, bool chunk_first) {  // S'_hf (+)= Z_hf^T P over the tile's 128 rows
         tc_fence_after();
 #pragma unroll 1
@@ -208,7 +214,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
           for (int kk = 0; kk < kTileM / 16; ++kk) {
             const uint32_t off = kk * 2048;  // 16 descriptor rows x 128 B
             mma_f16_ss_w(tmem + kWTS + kGW * hf, desc_sw128(za + off, kAtomBytes, 1024),
-                       desc_sw128(pb + off, kAtomBytes, 1024), idesc2, (chunk_first && s == 0 && kk == 0) ? 0u : 1u);
+                       desc_sw128(pb + off, kAtomBytes, 1024), hf == 1 ? idesc2b : idesc2,
+                       (chunk_first && s == 0 && kk == 0) ? 0u : 1u);
           }
         }
       };
@@ -251,7 +258,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         const int nrows = s_meta[i & 3].nrows;
         const uint8_t *xbox = smem + kWX + st * kXBoxBytes;
         if (bx == 3 && skip3) {
-        } else if (!kD128 || nrows < kTileM)
+        } else if (kPk && hf == 1)
+          zr_box<true, 16, 32>(xbox, row, bl, h, p.D - kDP, row < nrows, s_sc + kDP, s_ncs + kDP, ta);
+        else if (!kD128 || nrows < kTileM)
           zr_box<true>(xbox, row, bl, h, p.D - kDP * hf, row < nrows, s_sc + kDP * hf, s_ncs + kDP * hf, ta);
         else
           zr_box<false>(xbox, row, bl, h, kDP, true, s_sc + kDP * hf, s_ncs + kDP * hf, ta);
@@ -286,15 +295,32 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
         sts128(sZ + kOpBytes + kAtomBytes + o, zb[12], zb[13], zb[14], zb[15]);
       }
     };
+    auto copy_zb_packed = [&]() {  // kPk: Zr half b (lin hi 0-15 | quad hi 16-31 | lo + 32) -> atom 0 of Z
+      const uint32_t ta = tmem + kWTZr + 128 + lane_base;
+      uint32_t z[16];
+      tmem_ld4(ta + 4 * h, *reinterpret_cast<uint32_t(*)[4]>(z + 0));        // lin hi  dims 8h..
+      tmem_ld4(ta + 16 + 4 * h, *reinterpret_cast<uint32_t(*)[4]>(z + 4));   // quad hi
+      tmem_ld4(ta + 32 + 4 * h, *reinterpret_cast<uint32_t(*)[4]>(z + 8));   // lin lo
+      tmem_ld4(ta + 48 + 4 * h, *reinterpret_cast<uint32_t(*)[4]>(z + 12));  // quad lo
+      tmem_ld_wait(z);
+      sts128(sZ + sw_off(row, h), z[0], z[1], z[2], z[3]);
+      sts128(sZ + sw_off(row, 4 + h), z[4], z[5], z[6], z[7]);
+      sts128(sZ + kOpBytes + sw_off(row, h), z[8], z[9], z[10], z[11]);
+      sts128(sZ + kOpBytes + sw_off(row, 4 + h), z[12], z[13], z[14], z[15]);
+    };
     // S'_hf quarter (lane = half feature, columns 16h..) -> segment slot rows [lin 0..127 | quad 0..127]
     auto fold = [&](int b, bool first) {
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-        const int f = (row < kDP) ? kDP * hf + row : kDMax + kDP * hf + (row - kDP);
+        int f = (row < kDP) ? kDP * hf + row : kDMax + kDP * hf + (row - kDP);
+        // packed half b (M = 64): feature fp = 16 q + lane sits in lane 32 q + lane, lane < 16
+        const int fp = 16 * q + lane;
+        if (kPk && hf == 1) f = fp < 32 ? kDP + fp : kDMax + kDP + (fp - 32);
         float *dst = p.slots + (size_t)seg_slot(cid, b) * (2 * kDMax) * p.Kp + (size_t)f * p.Kp + rank * kGW + 16 * h;
         uint32_t v[16];
         tmem_ld16(tmem + kWTS + kGW * hf + lane_base + 16 * h, v);
         tmem_ld_wait(v);
+        if (kPk && hf == 1 && lane >= 16) continue;
         if (first) {
           float4 *d4 = reinterpret_cast<float4 *>(dst);
 #pragma unroll
@@ -315,7 +341,7 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
     for (int j = 0; j < 16; ++j) s0acc[j] = 0.f;
     int prev_b = 0;
     bool prev_fold = false, chunk_seg_first = true;
-    if (n > 0 && skip3) {  // the Zr columns of dims 96..127 (box 3 of half b) stay zero for the whole run
+    if (!kPk && n > 0 && skip3) {  // the Zr columns of dims 96..127 (box 3 of half b) stay zero for the whole run
       const uint32_t zero4[4] = {0u, 0u, 0u, 0u};
       const uint32_t ta = tmem + kWTZr + 128 + lane_base + 16 + 4 * h;
       tmem_st4(ta, zero4); tmem_st4(ta + 32, zero4); tmem_st4(ta + 64, zero4); tmem_st4(ta + 96, zero4);
@@ -455,7 +481,8 @@ __global__ void __launch_bounds__(kThreads2, 1) k_stats_w(const __grid_constant_
       TRW(8);
       work_wait(&bars[W_G2A_DONE], i & 1);  // GEMM2a(i) done reading Z
       TRW(9);
-      copy_z(1);
+      if (kPk) copy_zb_packed();
+      else copy_z(1);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
